@@ -1,0 +1,146 @@
+/*
+ * solomon_b200 -- B200 (sm_100a) drop-in for the two offloaded kernels of
+ * arXiv 2411.18889 (Miki & Hanawa, "Solomon"): the direct-summation N-body
+ * force `calc_acc` and the 7-point 3D diffusion step `diffusion3d`, plus the
+ * leapfrog (KDK) integrator the north star adds.
+ *
+ * Two layers, both plain C ABI (no CUDA or torch types in any signature):
+ *
+ * 1. Drop-in entry points with the reference's EXACT signatures. They accept
+ *    host pointers (the reference's fallback/OpenMP calling convention:
+ *    staged through device memory, synchronous on return) or device pointers
+ *    (the OpenACC `present(...)` convention: computed in place, synchronous).
+ *
+ * 2. Stream-ordered `b2_*` API on device pointers: no allocation, no host
+ *    synchronisation, returns 0 or an error code. Stateless and reentrant;
+ *    scratch space is caller-owned (`*_workspace_bytes`).
+ *
+ * Layouts are the reference's: particles are AoS float4 {x, y, z, m}
+ * (listing_nbody.c:1,4-5,9); accelerations float4 {ax, ay, az, pot|0}
+ * (listing_nbody.c:6,25); grids are float[nx*ny*nz] with
+ * INDEX = k + nz*(j + ny*i), k fastest (listing_diffusion.c:1).
+ */
+#ifndef SOLOMON_B200_H
+#define SOLOMON_B200_H
+
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(__VECTOR_TYPES_H__) || defined(__CUDACC__)
+typedef float4 solomon_float4;
+#else
+typedef struct solomon_float4 {
+  float x, y, z, w;
+} solomon_float4;
+#endif
+
+/* ---- return codes of the b2_* API --------------------------------------- */
+#define B2_OK 0
+#define B2_EINVAL (-1)  /* bad size / null pointer / unsupported flag        */
+#define B2_EALIGN (-2)  /* pointer not 16-byte aligned                       */
+#define B2_ESPACE (-3)  /* workspace too small                               */
+#define B2_ENOMEM (-4)  /* drop-in layer could not allocate staging memory   */
+/* positive values are cudaError_t codes from the launch / copy              */
+
+/* ---- b2_calc_acc flags --------------------------------------------------- */
+#define B2_POTENTIAL 1 /* also accumulate .w += m_j/sqrt(r2): listing_nbody.c:21-23 */
+#define B2_EXACT 2     /* IEEE 1/sqrt and the reference's sequential j order:
+                          bit-identical to the reference's -O3 fallback build  */
+
+/* =========================================================================
+ * 1. Drop-in entry points (reference signatures)
+ * ========================================================================= */
+
+/* Replaces `void calc_acc(const int Ni, float4 *ipos, float4 *iacc,
+ *                         const int Nj, float4 *jpos, const float eps)`
+ * -- pkg/tests/fixtures/listing_nbody.c:1. Host or device
+ * pointers; synchronous. Fast path (rsqrt.approx, j-chunked sums): results
+ * agree with the reference to FP32 tolerance. */
+void calc_acc(const int Ni, solomon_float4 *ipos, solomon_float4 *iacc, const int Nj,
+              solomon_float4 *jpos, const float eps);
+
+/* The same listing built with -DCALCULATE_POTENTIAL (listing_nbody.c:21-23). */
+void calc_acc_potential(const int Ni, solomon_float4 *ipos, solomon_float4 *iacc, const int Nj,
+                        solomon_float4 *jpos, const float eps);
+
+/* Replaces `void diffusion3d(int nx, int ny, int nz, float dx, float dy,
+ *   float dz, float dt, float kappa, const float *restrict f, float *restrict fn)`
+ * -- pkg/tests/fixtures/listing_diffusion.c:5. Host or device
+ * pointers; synchronous; bit-identical to the reference's -O3 build. */
+void diffusion3d(int nx, int ny, int nz, float dx, float dy, float dz, float dt, float kappa,
+                 const float *f, float *fn);
+
+/* Status of the last drop-in call on this thread (the reference's functions
+ * are void; this is how the drop-in reports failures -- also on stderr). */
+int b2_last_error(void);
+const char *b2_error_string(int code);
+const char *b2_version(void);
+
+/* =========================================================================
+ * 2. Stream-ordered API (device pointers; `stream` is a cudaStream_t or NULL)
+ * ========================================================================= */
+
+/* --- N-body force (listing_nbody.c:1-27) --- */
+
+/* Number of j-chunks the fast path splits Nj into. Depends on Nj and flags
+ * only, so a sharded run (different Ni) sums in the same order as an
+ * unsharded one. 1 for B2_EXACT. */
+int b2_calc_acc_nchunks(int Nj, int flags);
+
+/* Scratch bytes b2_calc_acc needs (0 when nchunks == 1). */
+size_t b2_calc_acc_workspace_bytes(int Ni, int Nj, int flags);
+
+/* iacc[i] = sum_j m_j (r_j - r_i) / (|r_j - r_i|^2 + eps^2)^{3/2}, i < Ni. */
+int b2_calc_acc(int Ni, const float *ipos, float *iacc, int Nj, const float *jpos, float eps,
+                int flags, void *workspace, size_t workspace_bytes, void *stream);
+
+/* Per-chunk partial sums: partials[c*Ni + i], c < b2_calc_acc_nchunks(Nj, flags).
+ * The building block the fused leapfrog update consumes. */
+int b2_calc_acc_partials(int Ni, const float *ipos, int Nj, const float *jpos, float eps, int flags,
+                         float *partials, void *stream);
+
+/* --- Leapfrog kick-drift-kick (no reference counterpart) --- */
+
+#define B2_KDK_REDUCE 1     /* acc = sum_c partials[c]  (fixed order c = 0..nchunks-1) */
+#define B2_KDK_KICK_END 2   /* vel.xyz = fma(acc, h_end, vel)   closing half-kick        */
+#define B2_KDK_KICK_DRIFT 4 /* vel.xyz = fma(acc, h_begin, vel); pos.xyz = fma(vel, dt, pos) */
+
+/* Fused per-particle update; phases run in the order listed above. */
+int b2_kdk_update(int n, float *pos, float *vel, float *acc, const float *partials, int nchunks,
+                  float h_end, float h_begin, float dt, int phases, void *stream);
+
+/* Whole single-device leapfrog: nsteps KDK steps of the self-gravitating
+ * system pos[n] (acc must hold a(pos) on entry unless B2_INIT_ACC is set;
+ * holds a(pos) on exit). Two kernel launches per step. */
+#define B2_INIT_ACC 4
+int b2_leapfrog(int n, float *pos, float *vel, float *acc, float eps, float dt, int nsteps, int flags,
+                void *workspace, size_t workspace_bytes, void *stream);
+size_t b2_leapfrog_workspace_bytes(int n, int flags);
+
+/* --- 3D diffusion (listing_diffusion.c:1-25) --- */
+
+/* One explicit step fn = L(f) over the whole grid; f != fn. */
+int b2_diffusion3d(int nx, int ny, int nz, float dx, float dy, float dz, float dt, float kappa,
+                   const float *f, float *fn, void *stream);
+
+/* Slab variant for i-decomposition: f holds this rank's
+ * nx_local planes; halo_lo / halo_hi are the neighbour planes i = -1 and
+ * i = nx_local (ny*nz floats each) or NULL at a global boundary (clamp, as
+ * IMAX(i-1,0) / IMIN(i+1,nx-1)). Computes output planes [i_begin, i_end). */
+int b2_diffusion3d_slab(int nx_local, int ny, int nz, float dx, float dy, float dz, float dt,
+                        float kappa, const float *f, const float *halo_lo, const float *halo_hi,
+                        float *fn, int i_begin, int i_end, void *stream);
+
+/* nsteps device-resident steps ping-ponging f <-> fn (no host sync). The
+ * result is in fn when nsteps is odd, in f when it is even. */
+int b2_diffusion3d_run(int nx, int ny, int nz, float dx, float dy, float dz, float dt, float kappa,
+                       float *f, float *fn, int nsteps, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SOLOMON_B200_H */

@@ -1,0 +1,93 @@
+"""ctypes binding of ``lib/libsolomon_b200.so`` (the sm_100a C-ABI, include/solomon_b200.h).
+
+There is no CPU fallback: if the library is missing or no CUDA device is
+visible, every compute call raises. ``load()`` is the single entry point.
+"""
+from __future__ import annotations
+
+import ctypes
+import pathlib
+import threading
+
+import torch
+
+PKG = pathlib.Path(__file__).resolve().parent
+LIB_PATH = PKG / "lib" / "libsolomon_b200.so"
+
+# include/solomon_b200.h
+B2_OK = 0
+B2_EINVAL = -1
+B2_EALIGN = -2
+B2_ESPACE = -3
+B2_ENOMEM = -4
+B2_POTENTIAL = 1
+B2_EXACT = 2
+B2_INIT_ACC = 4
+B2_KDK_REDUCE = 1
+B2_KDK_KICK_END = 2
+B2_KDK_KICK_DRIFT = 4
+
+_i, _f, _p, _sz = ctypes.c_int, ctypes.c_float, ctypes.c_void_p, ctypes.c_size_t
+
+# name -> (restype, argtypes); every symbol include/solomon_b200.h declares.
+SIGNATURES = {
+    "calc_acc": (None, [_i, _p, _p, _i, _p, _f]),
+    "calc_acc_potential": (None, [_i, _p, _p, _i, _p, _f]),
+    "diffusion3d": (None, [_i, _i, _i, _f, _f, _f, _f, _f, _p, _p]),
+    "b2_last_error": (_i, []),
+    "b2_error_string": (ctypes.c_char_p, [_i]),
+    "b2_version": (ctypes.c_char_p, []),
+    "b2_calc_acc_nchunks": (_i, [_i, _i]),
+    "b2_calc_acc_workspace_bytes": (_sz, [_i, _i, _i]),
+    "b2_calc_acc": (_i, [_i, _p, _p, _i, _p, _f, _i, _p, _sz, _p]),
+    "b2_calc_acc_partials": (_i, [_i, _p, _i, _p, _f, _i, _p, _p]),
+    "b2_kdk_update": (_i, [_i, _p, _p, _p, _p, _i, _f, _f, _f, _i, _p]),
+    "b2_leapfrog": (_i, [_i, _p, _p, _p, _f, _f, _i, _i, _p, _sz, _p]),
+    "b2_leapfrog_workspace_bytes": (_sz, [_i, _i]),
+    "b2_diffusion3d": (_i, [_i, _i, _i, _f, _f, _f, _f, _f, _p, _p, _p]),
+    "b2_diffusion3d_slab": (_i, [_i, _i, _i, _f, _f, _f, _f, _f, _p, _p, _p, _p, _i, _i, _p]),
+    "b2_diffusion3d_run": (_i, [_i, _i, _i, _f, _f, _f, _f, _f, _p, _p, _i, _p]),
+}
+
+_lock = threading.Lock()
+_lib: ctypes.CDLL | None = None
+
+
+class SolomonError(RuntimeError):
+    """A b2_* call returned a non-zero status."""
+
+
+def load(path: pathlib.Path | str | None = None) -> ctypes.CDLL:
+    """Load (once) and type the C-ABI library. Raises if it is missing."""
+    global _lib
+    with _lock:
+        if _lib is not None and path is None:
+            return _lib
+        p = pathlib.Path(path) if path else LIB_PATH
+        if not p.exists():
+            raise SolomonError(
+                f"{p} not found: build it with `python -m paper_2411_18889_b200.build` "
+                "(or __graft_entry__.build()); there is no CPU fallback")
+        lib = ctypes.CDLL(str(p))
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        if path is None:
+            _lib = lib
+        return lib
+
+
+def check(rc: int, what: str) -> None:
+    if rc != B2_OK:
+        msg = load().b2_error_string(rc).decode()
+        raise SolomonError(f"{what}: {msg} (code {rc})")
+
+
+def require_cuda(t: torch.Tensor, name: str) -> None:
+    if not t.is_cuda:
+        raise SolomonError(f"{name} must be a CUDA tensor (no CPU fallback); got device {t.device}")
+
+
+def stream_handle(device: torch.device | None = None) -> int:
+    return torch.cuda.current_stream(device).cuda_stream

@@ -1,0 +1,380 @@
+// K3: one explicit 7-point diffusion step (diffusion3d), hand-written for sm_100a.
+//
+// Reference: pkg/tests/fixtures/listing_diffusion.c:1-25 (= PAPER.md:553-578).
+//   INDEX(nx,ny,nz,i,j,k) = k + nz*(j + ny*i)        (:1)  k fastest, i slowest
+//   ce=cw=kappa*dt/dx^2, cn=cs=kappa*dt/dy^2, ct=cb=kappa*dt/dz^2, cc=1-sum (:6-9)
+//   fn = cc*f + ce*f[i+1] + cw*f[i-1] + cn*f[j+1] + cs*f[j-1] + ct*f[k+1] + cb*f[k-1]
+//   with neighbour indices clamped to the grid (:15-20).
+//
+// Design: HBM-bound (8 B/cell algorithmic). Each CTA owns a
+// tile of TJ full-width rows (j0..j0+TJ-1, all k) and marches along i (the
+// slowest, plane-contiguous axis) over a range of planes. A tile-plane plus
+// its j-1/j+1 halo rows is ONE contiguous run of (TJ+2)*nz floats, so it is
+// fetched with a single cp.async.bulk (UBLKCP, the TMA bulk-copy engine) into
+// an NST-deep shared-memory ring completed on mbarriers. Each thread keeps the
+// f[i-1] and f[i] values of its cells in registers, reads f[i+1] and the
+// in-plane neighbours from shared memory, and streams fn out with 16-byte
+// stores -- every f value crosses HBM once. The clamp of :15-20 is applied in
+// the kernel (TMA does not clamp). The arithmetic is the reference's as g++
+// -O3 contracts it: v = ce*f_ip; v = fma(cc, f, v); then
+// fma(cw,f_im), fma(cn,f_jp), fma(cs,f_jm), fma(ct,f_kp), fma(cb,f_km) --
+// bit-identical to the reference build.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+
+#include "common.cuh"
+
+namespace b2 {
+
+struct Coefs {
+  float cc, ce, cn, ct;
+};
+
+// listing_diffusion.c:6-9, evaluated in the same order as the reference build.
+static Coefs make_coefs(float dx, float dy, float dz, float dt, float kappa) {
+  volatile float kd = kappa * dt;  // volatile: keep every FP32 rounding on the host too
+  volatile float ce = kd / (dx * dx);
+  volatile float cn = kd / (dy * dy);
+  volatile float ct = kd / (dz * dz);
+  volatile float s = ce + ce;
+  s = s + cn;
+  s = s + cn;
+  s = s + ct;
+  s = s + ct;
+  Coefs c;
+  c.cc = 1.0f - s;
+  c.ce = ce;
+  c.cn = cn;
+  c.ct = ct;
+  return c;
+}
+
+__device__ __forceinline__ float cell(const Coefs& c, float fc, float fip, float fim, float fjp, float fjm, float fkp,
+                                      float fkm) {
+  float v = __fmul_rn(c.ce, fip);
+  v = __fmaf_rn(c.cc, fc, v);
+  v = __fmaf_rn(c.ce, fim, v);  // cw = ce
+  v = __fmaf_rn(c.cn, fjp, v);
+  v = __fmaf_rn(c.cn, fjm, v);  // cs = cn
+  v = __fmaf_rn(c.ct, fkp, v);
+  v = __fmaf_rn(c.ct, fkm, v);  // cb = ct
+  return v;
+}
+
+// ---- PTX helpers: mbarrier + bulk async copy (sm_90+/sm_100a) -------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+__device__ __forceinline__ void st_stream(float4* p, float4 v) { __stcs(p, v); }
+
+// ---------------------------------------------------------------------------
+// Marching kernel. Template S = float4 cells per thread per plane (registers).
+// Runtime: TJ rows per tile (TJ*nz/4 <= 256*S), NST pipeline stages.
+constexpr int kMarchThreads = 256;
+
+struct MarchArgs {
+  const float* f;        // local planes [0, nx)
+  const float* halo_lo;  // plane -1 or null (clamp)
+  const float* halo_hi;  // plane nx or null (clamp)
+  float* fn;
+  int nx, ny, nz;
+  int TJ, n_jtiles;
+  int i_begin, i_end, IC;  // output planes [i_begin, i_end), IC planes per CTA
+  int nst;
+  Coefs c;
+};
+
+template <int S>
+__global__ void __launch_bounds__(kMarchThreads, 2) k_diffusion_march(const MarchArgs a) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const int nz = a.nz, ny = a.ny, nx = a.nx;
+  const int nz4 = nz >> 2;
+  const int TJ = a.TJ, NST = a.nst;
+  const size_t plane = static_cast<size_t>(ny) * nz;
+  const int stage_floats = (TJ + 2) * nz;
+
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw);
+  float* stages = reinterpret_cast<float*>(smem_raw + 128);
+
+  const int jt = blockIdx.x % a.n_jtiles;
+  const int ic = blockIdx.x / a.n_jtiles;
+  const int j0 = jt * TJ;
+  const int rows = min(TJ, ny - j0);
+  const int i0 = a.i_begin + ic * a.IC;
+  const int i1 = min(i0 + a.IC, a.i_end);
+  if (i0 >= i1) return;  // uniform per CTA
+  const int L = (i1 - i0) + 2;  // planes to fetch: i0-1 .. i1
+
+  const int jlo = max(j0 - 1, 0);
+  const int jhi = min(j0 + rows, ny - 1);  // inclusive
+  const uint32_t bytes = static_cast<uint32_t>((jhi - jlo + 1) * nz * sizeof(float));
+  const int dst_row = jlo - (j0 - 1);  // buffer row q <-> global row j0-1+q
+
+  auto plane_src = [&](int p) -> const float* {
+    if (p < 0) return a.halo_lo ? a.halo_lo : a.f;  // IMAX(i-1, 0)
+    if (p >= nx) return a.halo_hi ? a.halo_hi : a.f + static_cast<size_t>(nx - 1) * plane;  // IMIN(i+1, nx-1)
+    return a.f + static_cast<size_t>(p) * plane;
+  };
+  auto issue = [&](int q) {  // fetch plane i0-1+q into stage q % NST
+    const int st = q % NST;
+    uint64_t* bar = bars + st;
+    mbar_expect_tx(bar, bytes);
+    bulk_g2s(stages + static_cast<size_t>(st) * stage_floats + dst_row * nz,
+             plane_src(i0 - 1 + q) + static_cast<size_t>(jlo) * nz, bytes, bar);
+  };
+
+  if (threadIdx.x == 0) {
+    for (int st = 0; st < NST; ++st) mbar_init(bars + st, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    const int pre = min(NST, L);
+    for (int q = 0; q < pre; ++q) issue(q);
+  }
+  __syncthreads();
+
+  // Per-thread cell positions within the tile.
+  int srow[S], scol[S];
+  bool sval[S];
+#pragma unroll
+  for (int s = 0; s < S; ++s) {
+    const int pos = threadIdx.x + s * kMarchThreads;
+    srow[s] = pos / nz4;
+    scol[s] = pos - srow[s] * nz4;
+    sval[s] = srow[s] < rows;
+  }
+
+  auto stage_ptr = [&](int q) -> const float* { return stages + static_cast<size_t>(q % NST) * stage_floats; };
+  auto wait_q = [&](int q) { mbar_wait(bars + (q % NST), (q / NST) & 1); };
+  auto own = [&](const float* buf, int s) -> float4 {
+    return *reinterpret_cast<const float4*>(buf + (srow[s] + 1) * nz + 4 * scol[s]);
+  };
+
+  float4 fim[S], fc[S];
+  // q = 0: plane i0-1 -> f[i-1] registers; release its stage.
+  wait_q(0);
+#pragma unroll
+  for (int s = 0; s < S; ++s)
+    if (sval[s]) fim[s] = own(stage_ptr(0), s);
+  __syncthreads();
+  if (threadIdx.x == 0 && NST < L) {
+    fence_proxy_async();
+    issue(NST);
+  }
+  // q = 1: plane i0 -> f[i] registers (stage kept for the in-plane neighbours).
+  wait_q(1);
+#pragma unroll
+  for (int s = 0; s < S; ++s)
+    if (sval[s]) fc[s] = own(stage_ptr(1), s);
+
+  const Coefs c = a.c;
+  for (int q = 1; q + 1 < L; ++q) {
+    const int p = i0 + q - 1;  // output plane
+    const float* cur = stage_ptr(q);
+    wait_q(q + 1);
+    const float* nxt = stage_ptr(q + 1);
+#pragma unroll
+    for (int s = 0; s < S; ++s) {
+      if (!sval[s]) continue;
+      const int r = srow[s], c4 = scol[s];
+      const int j = j0 + r;
+      const float4 fip = own(nxt, s);
+      const int rjp = min(j + 1, ny - 1) - (j0 - 1);
+      const int rjm = max(j - 1, 0) - (j0 - 1);
+      const float4 fjp = *reinterpret_cast<const float4*>(cur + rjp * nz + 4 * c4);
+      const float4 fjm = *reinterpret_cast<const float4*>(cur + rjm * nz + 4 * c4);
+      const float* rowp = cur + (r + 1) * nz;
+      const float4 fcv = fc[s];
+      const float kl = c4 > 0 ? rowp[4 * c4 - 1] : fcv.x;         // IMAX(k-1, 0)
+      const float kr = c4 + 1 < nz4 ? rowp[4 * c4 + 4] : fcv.w;   // IMIN(k+1, nz-1)
+      const float4 fm = fim[s];
+      float4 o;
+      o.x = cell(c, fcv.x, fip.x, fm.x, fjp.x, fjm.x, fcv.y, kl);
+      o.y = cell(c, fcv.y, fip.y, fm.y, fjp.y, fjm.y, fcv.z, fcv.x);
+      o.z = cell(c, fcv.z, fip.z, fm.z, fjp.z, fjm.z, fcv.w, fcv.y);
+      o.w = cell(c, fcv.w, fip.w, fm.w, fjp.w, fjm.w, kr, fcv.z);
+      st_stream(reinterpret_cast<float4*>(a.fn + static_cast<size_t>(p) * plane + static_cast<size_t>(j) * nz) + c4, o);
+      fim[s] = fcv;
+      fc[s] = fip;
+    }
+    __syncthreads();  // everyone is done with stage q
+    if (threadIdx.x == 0 && q + NST < L) {
+      fence_proxy_async();
+      issue(q + NST);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Generic kernel for shapes the marching kernel does not take (nz % 4 != 0,
+// unaligned pointers). One thread per cell, 64-bit offsets.
+__global__ void __launch_bounds__(256)
+    k_diffusion_generic(const float* __restrict__ f, const float* __restrict__ halo_lo,
+                        const float* __restrict__ halo_hi, float* __restrict__ fn, int nx, int ny, int nz, int i_begin,
+                        int i_end, Coefs c) {
+  const size_t plane = static_cast<size_t>(ny) * nz;
+  const size_t total = static_cast<size_t>(i_end - i_begin) * plane;
+  for (size_t t = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; t < total;
+       t += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    const int i = i_begin + static_cast<int>(t / plane);
+    const size_t r = t % plane;
+    const int j = static_cast<int>(r / nz);
+    const int k = static_cast<int>(r % nz);
+    const float* P = f + static_cast<size_t>(i) * plane;
+    const float* Pm = i > 0 ? P - plane : (halo_lo ? halo_lo : P);
+    const float* Pp = i < nx - 1 ? P + plane : (halo_hi ? halo_hi : P);
+    const size_t jk = static_cast<size_t>(j) * nz + k;
+    const float fc = P[jk];
+    const float fjp = P[static_cast<size_t>(min(j + 1, ny - 1)) * nz + k];
+    const float fjm = P[static_cast<size_t>(max(j - 1, 0)) * nz + k];
+    const float fkp = P[static_cast<size_t>(j) * nz + min(k + 1, nz - 1)];
+    const float fkm = P[static_cast<size_t>(j) * nz + max(k - 1, 0)];
+    fn[static_cast<size_t>(i) * plane + jk] = cell(c, fc, Pp[jk], Pm[jk], fjp, fjm, fkp, fkm);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Host planning.
+struct MarchPlan {
+  int S = 0, TJ = 0, nst = 0, n_jtiles = 0, IC = 0, grid = 0;
+  size_t smem = 0;
+};
+
+static bool plan_march(int nx_out, int ny, int nz, MarchPlan& mp) {
+  if (nz % 4 != 0 || nz < 4) return false;
+  const int nz4 = nz / 4;
+  const DeviceInfo& di = device_info();
+  // Choose S (cells/thread/4) so a tile has >= 2 rows and fits 3+ stages in
+  // half the SM's shared memory (two CTAs per SM).
+  static const int kS[] = {4, 8, 2, 1};
+  for (int S : kS) {
+    int TJ = (kMarchThreads * S) / nz4;
+    if (TJ < 1) continue;
+    TJ = std::min(TJ, ny);
+    const size_t stage = static_cast<size_t>(TJ + 2) * nz * sizeof(float);
+    const size_t budget = std::min<size_t>(di.smem_optin, 227 * 1024) / 2 - 128;
+    int nst = static_cast<int>(std::min<size_t>(4, budget / stage));
+    if (nst < 2) continue;
+    mp.S = S;
+    mp.TJ = TJ;
+    mp.nst = nst;
+    mp.smem = 128 + stage * nst;
+    break;
+  }
+  if (!mp.S) return false;
+  mp.n_jtiles = (ny + mp.TJ - 1) / mp.TJ;
+  // Single co-resident wave when possible: split i so that n_jtiles * splits
+  // fills the 2-CTA-per-SM residency; neighbours then march in lock step and
+  // share halo rows/planes through L2.
+  const int resident = 2 * di.sms;
+  int splits = std::max(1, resident / mp.n_jtiles);
+  splits = std::min(splits, std::max(1, nx_out / 4));
+  mp.IC = (nx_out + splits - 1) / splits;
+  mp.grid = mp.n_jtiles * ((nx_out + mp.IC - 1) / mp.IC);
+  return true;
+}
+
+static int launch_step(int nx, int ny, int nz, const Coefs& c, const float* f, const float* lo, const float* hi,
+                       float* fn, int i_begin, int i_end, cudaStream_t s) {
+  if (i_end <= i_begin) return B2_OK;
+  MarchPlan mp;
+  const bool ok_align = aligned16(f) && aligned16(fn) && (!lo || aligned16(lo)) && (!hi || aligned16(hi));
+  if (ok_align && plan_march(i_end - i_begin, ny, nz, mp)) {
+    MarchArgs a{f, lo, hi, fn, nx, ny, nz, mp.TJ, mp.n_jtiles, i_begin, i_end, mp.IC, mp.nst, c};
+    switch (mp.S) {
+#define B2_MARCH_CASE(SV)                                                                                     \
+  case SV: {                                                                                                  \
+    static bool attr_set = false;                                                                             \
+    if (!attr_set) {                                                                                          \
+      cudaFuncSetAttribute(k_diffusion_march<SV>, cudaFuncAttributeMaxDynamicSharedMemorySize, 113 * 1024); \
+      attr_set = true;                                                                                        \
+    }                                                                                                         \
+    k_diffusion_march<SV><<<mp.grid, kMarchThreads, mp.smem, s>>>(a);                                         \
+    break;                                                                                                    \
+  }
+      B2_MARCH_CASE(1)
+      B2_MARCH_CASE(2)
+      B2_MARCH_CASE(4)
+      B2_MARCH_CASE(8)
+#undef B2_MARCH_CASE
+      default:
+        return B2_EINVAL;
+    }
+    return launch_status();
+  }
+  const size_t total = static_cast<size_t>(i_end - i_begin) * ny * nz;
+  const int grid = static_cast<int>(std::min<size_t>((total + 255) / 256, 148 * 64));
+  k_diffusion_generic<<<grid, 256, 0, s>>>(f, lo, hi, fn, nx, ny, nz, i_begin, i_end, c);
+  return launch_status();
+}
+
+static int check_grid(int nx, int ny, int nz, const float* f, const float* fn) {
+  if (nx <= 0 || ny <= 0 || nz <= 0 || !f || !fn) return B2_EINVAL;
+  if (f == fn) return B2_EINVAL;  // restrict: listing_diffusion.c:5
+  return B2_OK;
+}
+
+}  // namespace b2
+
+using namespace b2;
+
+extern "C" {
+
+int b2_diffusion3d(int nx, int ny, int nz, float dx, float dy, float dz, float dt, float kappa, const float* f,
+                   float* fn, void* stream) {
+  if (int rc = check_grid(nx, ny, nz, f, fn)) return rc;
+  return launch_step(nx, ny, nz, make_coefs(dx, dy, dz, dt, kappa), f, nullptr, nullptr, fn, 0, nx,
+                     as_stream(stream));
+}
+
+int b2_diffusion3d_slab(int nx_local, int ny, int nz, float dx, float dy, float dz, float dt, float kappa,
+                        const float* f, const float* halo_lo, const float* halo_hi, float* fn, int i_begin, int i_end,
+                        void* stream) {
+  if (int rc = check_grid(nx_local, ny, nz, f, fn)) return rc;
+  if (i_begin < 0 || i_end > nx_local || i_begin > i_end) return B2_EINVAL;
+  return launch_step(nx_local, ny, nz, make_coefs(dx, dy, dz, dt, kappa), f, halo_lo, halo_hi, fn, i_begin, i_end,
+                     as_stream(stream));
+}
+
+int b2_diffusion3d_run(int nx, int ny, int nz, float dx, float dy, float dz, float dt, float kappa, float* f,
+                       float* fn, int nsteps, void* stream) {
+  if (int rc = check_grid(nx, ny, nz, f, fn)) return rc;
+  if (nsteps < 0) return B2_EINVAL;
+  const Coefs c = make_coefs(dx, dy, dz, dt, kappa);
+  cudaStream_t s = as_stream(stream);
+  float* a = f;
+  float* b = fn;
+  for (int st = 0; st < nsteps; ++st) {
+    if (int rc = launch_step(nx, ny, nz, c, a, nullptr, nullptr, b, 0, nx, s)) return rc;
+    std::swap(a, b);
+  }
+  return B2_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,184 @@
+// Drop-in layer: the reference's exact C signatures on top of the b2_* API.
+//
+//   calc_acc     -- pkg/tests/fixtures/listing_nbody.c:1
+//   diffusion3d  -- pkg/tests/fixtures/listing_diffusion.c:5
+//
+// The reference functions are synchronous and take whatever pointers the
+// backend implies: host memory under the fallback (host OpenMP) lowering,
+// device-present memory under OpenACC `present(f, fn)` (listing_diffusion.c:10,
+// conformance.rows:756). These entry points accept both: device/managed
+// pointers are used in place; host pointers are staged through a cached
+// device buffer. Either way the call returns when the result is in the
+// caller's buffer. Errors (the reference has none -- bad sizes are UB there)
+// are reported on stderr and through b2_last_error().
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <vector>
+
+#include "common.cuh"
+
+namespace b2 {
+
+static thread_local int g_last_error = B2_OK;
+
+const DeviceInfo& device_info() {
+  static DeviceInfo infos[64];
+  static bool ready[64] = {};
+  static std::mutex mu;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(mu);
+  if (!ready[dev]) {
+    cudaDeviceGetAttribute(&infos[dev].sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaDeviceGetAttribute(&infos[dev].smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    ready[dev] = true;
+  }
+  return infos[dev];
+}
+
+// Per-device staging arena for host-pointer calls (grown on demand, never shrunk).
+struct Arena {
+  void* ptr = nullptr;
+  size_t bytes = 0;
+  cudaStream_t stream = nullptr;
+};
+
+static std::mutex g_arena_mu;
+static Arena g_arena[64];
+
+static void* arena_get(size_t bytes, cudaStream_t* s) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  Arena& a = g_arena[dev];
+  if (!a.stream) cudaStreamCreateWithFlags(&a.stream, cudaStreamNonBlocking);
+  if (a.bytes < bytes) {
+    if (a.ptr) cudaFree(a.ptr);
+    a.ptr = nullptr;
+    a.bytes = 0;
+    if (cudaMalloc(&a.ptr, bytes) != cudaSuccess) return nullptr;
+    a.bytes = bytes;
+  }
+  *s = a.stream;
+  return a.ptr;
+}
+
+static bool is_device_ptr(const void* p) {
+  cudaPointerAttributes attr;
+  if (cudaPointerGetAttributes(&attr, p) != cudaSuccess) {
+    cudaGetLastError();  // clear: plain host pointers may report an error on old drivers
+    return false;
+  }
+  return attr.type == cudaMemoryTypeDevice || attr.type == cudaMemoryTypeManaged;
+}
+
+static size_t align_up(size_t x) { return (x + 255) & ~static_cast<size_t>(255); }
+
+static int report(const char* fn, int rc) {
+  g_last_error = rc;
+  if (rc != B2_OK) std::fprintf(stderr, "solomon_b200: %s failed: %s (%d)\n", fn, b2_error_string(rc), rc);
+  return rc;
+}
+
+static int calc_acc_dropin(int Ni, void* ipos, void* iacc, int Nj, void* jpos, float eps, int flags) {
+  if (Ni < 0 || Nj < 0 || (Ni > 0 && (!ipos || !iacc)) || (Nj > 0 && !jpos)) return B2_EINVAL;
+  if (Ni == 0) return B2_OK;
+  const bool dev = is_device_ptr(ipos) && is_device_ptr(iacc) && (Nj == 0 || is_device_ptr(jpos));
+  const size_t ws = b2_calc_acc_workspace_bytes(Ni, Nj, flags);
+  std::lock_guard<std::mutex> lk(g_arena_mu);
+  if (dev) {
+    cudaStream_t s;
+    void* w = ws ? arena_get(ws, &s) : (arena_get(256, &s));
+    if (!w) return B2_ENOMEM;
+    int rc = b2_calc_acc(Ni, static_cast<float*>(ipos), static_cast<float*>(iacc), Nj, static_cast<float*>(jpos), eps,
+                         flags, w, ws, s);
+    if (rc) return rc;
+    cudaError_t e = cudaStreamSynchronize(s);
+    return e == cudaSuccess ? B2_OK : static_cast<int>(e);
+  }
+  const size_t bi = align_up(sizeof(float4) * static_cast<size_t>(Ni));
+  const size_t bj = align_up(sizeof(float4) * static_cast<size_t>(Nj));
+  const bool same = ipos == jpos && Ni == Nj;
+  const size_t total = bi /*ipos*/ + bi /*iacc*/ + (same ? 0 : bj) + align_up(ws);
+  cudaStream_t s;
+  char* base = static_cast<char*>(arena_get(total, &s));
+  if (!base) return B2_ENOMEM;
+  float* d_i = reinterpret_cast<float*>(base);
+  float* d_a = reinterpret_cast<float*>(base + bi);
+  float* d_j = same ? d_i : reinterpret_cast<float*>(base + 2 * bi);
+  void* d_w = base + 2 * bi + (same ? 0 : bj);
+  cudaMemcpyAsync(d_i, ipos, sizeof(float4) * static_cast<size_t>(Ni), cudaMemcpyDefault, s);
+  if (!same && Nj) cudaMemcpyAsync(d_j, jpos, sizeof(float4) * static_cast<size_t>(Nj), cudaMemcpyDefault, s);
+  int rc = b2_calc_acc(Ni, d_i, d_a, Nj, d_j, eps, flags, d_w, ws, s);
+  if (rc) return rc;
+  cudaMemcpyAsync(iacc, d_a, sizeof(float4) * static_cast<size_t>(Ni), cudaMemcpyDefault, s);
+  cudaError_t e = cudaStreamSynchronize(s);
+  return e == cudaSuccess ? B2_OK : static_cast<int>(e);
+}
+
+static int diffusion_dropin(int nx, int ny, int nz, float dx, float dy, float dz, float dt, float kappa,
+                            const float* f, float* fn) {
+  if (nx <= 0 || ny <= 0 || nz <= 0 || !f || !fn || f == fn) return B2_EINVAL;
+  const size_t n = static_cast<size_t>(nx) * ny * nz;
+  std::lock_guard<std::mutex> lk(g_arena_mu);
+  if (is_device_ptr(f) && is_device_ptr(fn)) {
+    cudaStream_t s;
+    if (!arena_get(256, &s)) return B2_ENOMEM;
+    int rc = b2_diffusion3d(nx, ny, nz, dx, dy, dz, dt, kappa, f, fn, s);
+    if (rc) return rc;
+    cudaError_t e = cudaStreamSynchronize(s);
+    return e == cudaSuccess ? B2_OK : static_cast<int>(e);
+  }
+  const size_t b = align_up(n * sizeof(float));
+  cudaStream_t s;
+  char* base = static_cast<char*>(arena_get(2 * b, &s));
+  if (!base) return B2_ENOMEM;
+  float* d_f = reinterpret_cast<float*>(base);
+  float* d_fn = reinterpret_cast<float*>(base + b);
+  cudaMemcpyAsync(d_f, f, n * sizeof(float), cudaMemcpyDefault, s);
+  int rc = b2_diffusion3d(nx, ny, nz, dx, dy, dz, dt, kappa, d_f, d_fn, s);
+  if (rc) return rc;
+  cudaMemcpyAsync(fn, d_fn, n * sizeof(float), cudaMemcpyDefault, s);
+  cudaError_t e = cudaStreamSynchronize(s);
+  return e == cudaSuccess ? B2_OK : static_cast<int>(e);
+}
+
+}  // namespace b2
+
+using namespace b2;
+
+extern "C" {
+
+void calc_acc(const int Ni, solomon_float4* ipos, solomon_float4* iacc, const int Nj, solomon_float4* jpos,
+              const float eps) {
+  report("calc_acc", calc_acc_dropin(Ni, ipos, iacc, Nj, jpos, eps, 0));
+}
+
+void calc_acc_potential(const int Ni, solomon_float4* ipos, solomon_float4* iacc, const int Nj, solomon_float4* jpos,
+                        const float eps) {
+  report("calc_acc_potential", calc_acc_dropin(Ni, ipos, iacc, Nj, jpos, eps, B2_POTENTIAL));
+}
+
+void diffusion3d(int nx, int ny, int nz, float dx, float dy, float dz, float dt, float kappa, const float* f,
+                 float* fn) {
+  report("diffusion3d", diffusion_dropin(nx, ny, nz, dx, dy, dz, dt, kappa, f, fn));
+}
+
+int b2_last_error(void) { return g_last_error; }
+
+const char* b2_error_string(int code) {
+  switch (code) {
+    case B2_OK: return "ok";
+    case B2_EINVAL: return "invalid argument";
+    case B2_EALIGN: return "pointer not 16-byte aligned";
+    case B2_ESPACE: return "workspace too small";
+    case B2_ENOMEM: return "out of device memory";
+    default: return code > 0 ? cudaGetErrorString(static_cast<cudaError_t>(code)) : "unknown error";
+  }
+}
+
+const char* b2_version(void) { return "solomon_b200 0.1.0 (sm_100a)"; }
+
+}  // extern "C"

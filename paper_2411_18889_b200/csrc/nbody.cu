@@ -1,0 +1,383 @@
+// K1: direct-summation softened gravity (calc_acc) and K2: fused leapfrog
+// update, hand-written for sm_100a.
+//
+// Reference: pkg/tests/fixtures/listing_nbody.c:1-27 (= PAPER.md:467-493).
+//   for i < Ni:                 (parallel, :2-3)
+//     pi = ipos[i]; pi.w = eps^2                                  (:4-5)
+//     for j < Nj:               (sequential, :7-8)
+//       r  = pj - pi                                              (:11-13)
+//       r2 = fma(rz,rz, fma(ry,ry, fma(rx,rx, eps^2)))            (:14)
+//       w  = 1/sqrt(r2); w *= w*w; w *= m_j                       (:15-17)
+//       a += r*w  (3 FMA); [pot: a.w = fma(r2, w, a.w)]           (:18-23)
+//
+// Fast kernel design: FP32 CUDA-core work (not a contraction,
+// so no tensor cores). Each thread owns IPT=8 i-particles as 4 packed pairs
+// and evaluates every interaction with Blackwell's packed FP32 instructions
+// (FADD2/FFMA2/FMUL2 -- 6 issue slots per 2 interactions instead of 12) plus
+// MUFU.RSQ. j-particles stream through shared memory in BLOCK-sized tiles,
+// double-buffered, pre-duplicated as {x,x,y,y},{z,z,m,m} so one LDS.128 feeds
+// a packed operand pair with no MOVs. Nj is cut into fixed chunks whose size
+// depends on Nj only; each (i-tile, j-chunk) is one CTA of work, giving >50
+// waves at N=2^20 (no tail), and per-chunk partial sums are combined in a
+// fixed order by the K2 update kernel (deterministic, shard-invariant).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+#include <cstdio>
+
+#include "common.cuh"
+
+namespace b2 {
+
+constexpr int kIPT = 8;            // i-particles per thread (4 packed pairs)
+constexpr int kChunkAlign = 256;   // j-chunk sizes are multiples of this
+constexpr int kTargetChunks = 64;  // j-chunks per force evaluation (fast path)
+
+__device__ __forceinline__ float rsqrt_approx(float x) {
+  float r;
+  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+
+// ---------------------------------------------------------------------------
+// K1 fast: packed-FP32 tile kernel.
+// grid.x = n_itiles * nchunks; block = BLOCK threads; out = partials[c][Ni].
+template <int BLOCK, bool POT>
+__global__ void __launch_bounds__(BLOCK, (BLOCK >= 256 ? 2 : 8))
+    k_force_fast(const float4* __restrict__ ipos, int Ni, const float4* __restrict__ jpos, int Nj,
+                 int jchunk, int n_itiles, float eps2, float4* __restrict__ out) {
+  __shared__ float4 sj[2][2 * BLOCK];
+
+  const int tid = threadIdx.x;
+  const int itile = blockIdx.x % n_itiles;
+  const int chunk = blockIdx.x / n_itiles;
+  const int ibase = itile * (BLOCK * kIPT) + tid;
+
+  float2 nx[kIPT / 2], ny[kIPT / 2], nz[kIPT / 2];
+  float2 ax[kIPT / 2], ay[kIPT / 2], az[kIPT / 2], ap[kIPT / 2];
+#pragma unroll
+  for (int p = 0; p < kIPT / 2; ++p) {
+    const int ia = min(ibase + (2 * p) * BLOCK, Ni - 1);
+    const int ib = min(ibase + (2 * p + 1) * BLOCK, Ni - 1);
+    const float4 a = __ldg(ipos + ia), b = __ldg(ipos + ib);
+    // r = pj - pi computed as pj + (-pi): identical in IEEE arithmetic.
+    nx[p] = make_float2(-a.x, -b.x);
+    ny[p] = make_float2(-a.y, -b.y);
+    nz[p] = make_float2(-a.z, -b.z);
+    ax[p] = ay[p] = az[p] = ap[p] = make_float2(0.f, 0.f);
+  }
+  const float2 e2 = make_float2(eps2, eps2);
+
+  const int j0 = chunk * jchunk;
+  const int j1 = min(j0 + jchunk, Nj);
+  const int ntiles = (j1 - j0 + BLOCK - 1) / BLOCK;
+
+  // Padding j (beyond j1) gets m = 0 at the origin: contributes exactly 0
+  // whenever the reference itself is finite (eps > 0).
+  auto fetch = [&](int t) -> float4 {
+    const int j = j0 + t * BLOCK + tid;
+    return j < j1 ? __ldg(jpos + j) : make_float4(0.f, 0.f, 0.f, 0.f);
+  };
+  auto stash = [&](int buf, float4 pj) {
+    sj[buf][2 * tid + 0] = make_float4(pj.x, pj.x, pj.y, pj.y);
+    sj[buf][2 * tid + 1] = make_float4(pj.z, pj.z, pj.w, pj.w);
+  };
+
+  stash(0, fetch(0));
+  __syncthreads();
+
+  for (int t = 0; t < ntiles; ++t) {
+    const int buf = t & 1;
+    float4 next;
+    const bool more = (t + 1) < ntiles;
+    if (more) next = fetch(t + 1);
+
+    const float4* __restrict__ s = sj[buf];
+#pragma unroll 4
+    for (int jj = 0; jj < BLOCK; ++jj) {
+      const float4 A = s[2 * jj + 0];
+      const float4 B = s[2 * jj + 1];
+      const float2 X = make_float2(A.x, A.y);
+      const float2 Y = make_float2(A.z, A.w);
+      const float2 Z = make_float2(B.x, B.y);
+      const float2 M = make_float2(B.z, B.w);
+#pragma unroll
+      for (int p = 0; p < kIPT / 2; ++p) {
+        const float2 rx = __fadd2_rn(X, nx[p]);
+        const float2 ry = __fadd2_rn(Y, ny[p]);
+        const float2 rz = __fadd2_rn(Z, nz[p]);
+        float2 r2 = __ffma2_rn(rx, rx, e2);
+        r2 = __ffma2_rn(ry, ry, r2);
+        r2 = __ffma2_rn(rz, rz, r2);
+        float2 w = make_float2(rsqrt_approx(r2.x), rsqrt_approx(r2.y));
+        w = __fmul2_rn(w, __fmul2_rn(w, w));
+        w = __fmul2_rn(w, M);
+        ax[p] = __ffma2_rn(rx, w, ax[p]);
+        ay[p] = __ffma2_rn(ry, w, ay[p]);
+        az[p] = __ffma2_rn(rz, w, az[p]);
+        if (POT) ap[p] = __ffma2_rn(r2, w, ap[p]);
+      }
+    }
+    if (more) stash(buf ^ 1, next);
+    __syncthreads();
+  }
+
+  float4* __restrict__ o = out + static_cast<size_t>(chunk) * Ni;
+#pragma unroll
+  for (int p = 0; p < kIPT / 2; ++p) {
+    const int ia = ibase + (2 * p) * BLOCK;
+    const int ib = ibase + (2 * p + 1) * BLOCK;
+    if (ia < Ni) o[ia] = make_float4(ax[p].x, ay[p].x, az[p].x, POT ? ap[p].x : 0.f);
+    if (ib < Ni) o[ib] = make_float4(ax[p].y, ay[p].y, az[p].y, POT ? ap[p].y : 0.f);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K1 exact: the reference's arithmetic, bit for bit (IEEE sqrt and divide,
+// explicit roundings so nvcc cannot contract, sequential j). One i per thread.
+template <bool POT>
+__global__ void __launch_bounds__(128)
+    k_force_exact(const float4* __restrict__ ipos, int Ni, const float4* __restrict__ jpos, int Nj, float eps2,
+                  float4* __restrict__ out) {
+  constexpr int T = 128;
+  __shared__ float4 sj[T];
+  const int i = blockIdx.x * T + threadIdx.x;
+  const float4 pi = __ldg(ipos + min(i, Ni - 1));
+  float ax = 0.f, ay = 0.f, az = 0.f, aw = 0.f;
+  for (int jt = 0; jt < Nj; jt += T) {
+    const int cnt = min(T, Nj - jt);
+    __syncthreads();
+    if (threadIdx.x < cnt) sj[threadIdx.x] = __ldg(jpos + jt + threadIdx.x);
+    __syncthreads();
+    for (int jj = 0; jj < cnt; ++jj) {
+      const float4 pj = sj[jj];
+      const float rx = __fsub_rn(pj.x, pi.x);
+      const float ry = __fsub_rn(pj.y, pi.y);
+      const float rz = __fsub_rn(pj.z, pi.z);
+      const float r2 = __fmaf_rn(rz, rz, __fmaf_rn(ry, ry, __fmaf_rn(rx, rx, eps2)));
+      float w = __fdiv_rn(1.0f, __fsqrt_rn(r2));
+      w = __fmul_rn(w, __fmul_rn(w, w));
+      w = __fmul_rn(w, pj.w);
+      ax = __fmaf_rn(rx, w, ax);
+      ay = __fmaf_rn(ry, w, ay);
+      az = __fmaf_rn(rz, w, az);
+      if (POT) aw = __fmaf_rn(r2, w, aw);
+    }
+  }
+  if (i < Ni) out[i] = make_float4(ax, ay, az, aw);
+}
+
+// ---------------------------------------------------------------------------
+// K2: fused reduce + kick(s) + drift. One particle per thread, float4 I/O.
+__global__ void __launch_bounds__(256)
+    k_kdk_update(int n, float4* __restrict__ pos, float4* __restrict__ vel, float4* __restrict__ acc,
+                 const float4* __restrict__ partials, int nchunks, float h_end, float h_begin, float dt,
+                 int phases) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  float4 a;
+  if (phases & B2_KDK_REDUCE) {
+    a = __ldcs(partials + i);
+    for (int c = 1; c < nchunks; ++c) {
+      const float4 p = __ldcs(partials + static_cast<size_t>(c) * n + i);
+      a.x = __fadd_rn(a.x, p.x);
+      a.y = __fadd_rn(a.y, p.y);
+      a.z = __fadd_rn(a.z, p.z);
+      a.w = __fadd_rn(a.w, p.w);
+    }
+    acc[i] = a;
+  } else {
+    a = acc[i];
+  }
+  if (!(phases & (B2_KDK_KICK_END | B2_KDK_KICK_DRIFT))) return;
+  float4 v = vel[i];
+  if (phases & B2_KDK_KICK_END) {
+    v.x = __fmaf_rn(a.x, h_end, v.x);
+    v.y = __fmaf_rn(a.y, h_end, v.y);
+    v.z = __fmaf_rn(a.z, h_end, v.z);
+  }
+  if (phases & B2_KDK_KICK_DRIFT) {
+    v.x = __fmaf_rn(a.x, h_begin, v.x);
+    v.y = __fmaf_rn(a.y, h_begin, v.y);
+    v.z = __fmaf_rn(a.z, h_begin, v.z);
+    float4 x = pos[i];
+    x.x = __fmaf_rn(v.x, dt, x.x);
+    x.y = __fmaf_rn(v.y, dt, x.y);
+    x.z = __fmaf_rn(v.z, dt, x.z);
+    pos[i] = x;
+  }
+  vel[i] = v;
+}
+
+// ---------------------------------------------------------------------------
+// Host-side planning.
+
+static int chunk_size(int Nj, int flags) {
+  if (flags & B2_EXACT) return Nj;
+  int c = (Nj + kTargetChunks - 1) / kTargetChunks;
+  c = (c + kChunkAlign - 1) / kChunkAlign * kChunkAlign;
+  return std::max(c, kChunkAlign);
+}
+
+static int nchunks_for(int Nj, int flags) {
+  if (Nj <= 0) return 0;
+  const int c = chunk_size(Nj, flags);
+  return (Nj + c - 1) / c;
+}
+
+static int launch_partials(int Ni, const float4* ipos, int Nj, const float4* jpos, float eps, int flags,
+                           float4* out, cudaStream_t s) {
+  const float eps2 = eps * eps;  // listing_nbody.c:5
+  const bool pot = flags & B2_POTENTIAL;
+  if (flags & B2_EXACT) {
+    const int grid = (Ni + 127) / 128;
+    if (pot)
+      k_force_exact<true><<<grid, 128, 0, s>>>(ipos, Ni, jpos, Nj, eps2, out);
+    else
+      k_force_exact<false><<<grid, 128, 0, s>>>(ipos, Ni, jpos, Nj, eps2, out);
+    return launch_status();
+  }
+  const int jchunk = chunk_size(Nj, flags);
+  const int nch = nchunks_for(Nj, flags);
+  // Small i-sets use 64-thread CTAs so that the (i-tile, j-chunk) grid still
+  // covers the 148 SMs; large ones use 256-thread CTAs (2 per SM).
+  const bool small = static_cast<long long>((Ni + 256 * kIPT - 1) / (256 * kIPT)) * nch < 8LL * device_info().sms;
+  if (small) {
+    const int nit = (Ni + 64 * kIPT - 1) / (64 * kIPT);
+    const dim3 grid(nit * nch);
+    if (pot)
+      k_force_fast<64, true><<<grid, 64, 0, s>>>(ipos, Ni, jpos, Nj, jchunk, nit, eps2, out);
+    else
+      k_force_fast<64, false><<<grid, 64, 0, s>>>(ipos, Ni, jpos, Nj, jchunk, nit, eps2, out);
+  } else {
+    const int nit = (Ni + 256 * kIPT - 1) / (256 * kIPT);
+    const dim3 grid(nit * nch);
+    if (pot)
+      k_force_fast<256, true><<<grid, 256, 0, s>>>(ipos, Ni, jpos, Nj, jchunk, nit, eps2, out);
+    else
+      k_force_fast<256, false><<<grid, 256, 0, s>>>(ipos, Ni, jpos, Nj, jchunk, nit, eps2, out);
+  }
+  return launch_status();
+}
+
+static int launch_update(int n, float4* pos, float4* vel, float4* acc, const float4* partials, int nchunks,
+                         float h_end, float h_begin, float dt, int phases, cudaStream_t s) {
+  if (n <= 0) return B2_OK;
+  k_kdk_update<<<(n + 255) / 256, 256, 0, s>>>(n, pos, vel, acc, partials, nchunks, h_end, h_begin, dt, phases);
+  return launch_status();
+}
+
+static int check_particles(int n, const float* p) {
+  if (n < 0) return B2_EINVAL;
+  if (n > 0 && p == nullptr) return B2_EINVAL;
+  if (n > 0 && !aligned16(p)) return B2_EALIGN;
+  return B2_OK;
+}
+
+}  // namespace b2
+
+using namespace b2;
+
+extern "C" {
+
+int b2_calc_acc_nchunks(int Nj, int flags) { return nchunks_for(Nj, flags); }
+
+size_t b2_calc_acc_workspace_bytes(int Ni, int Nj, int flags) {
+  const int nch = nchunks_for(Nj, flags);
+  if (nch <= 1 || Ni <= 0) return 0;
+  return static_cast<size_t>(nch) * static_cast<size_t>(Ni) * sizeof(float4);
+}
+
+int b2_calc_acc_partials(int Ni, const float* ipos, int Nj, const float* jpos, float eps, int flags,
+                         float* partials, void* stream) {
+  int rc;
+  if ((rc = check_particles(Ni, ipos)) || (rc = check_particles(Nj, jpos)) || (rc = check_particles(Ni, partials)))
+    return rc;
+  if (flags & ~(B2_POTENTIAL | B2_EXACT)) return B2_EINVAL;
+  if (Ni == 0) return B2_OK;
+  if (Nj == 0) {
+    cudaMemsetAsync(partials, 0, sizeof(float4) * static_cast<size_t>(Ni), as_stream(stream));
+    return launch_status();
+  }
+  return launch_partials(Ni, reinterpret_cast<const float4*>(ipos), Nj, reinterpret_cast<const float4*>(jpos), eps,
+                         flags, reinterpret_cast<float4*>(partials), as_stream(stream));
+}
+
+int b2_calc_acc(int Ni, const float* ipos, float* iacc, int Nj, const float* jpos, float eps, int flags,
+                void* workspace, size_t workspace_bytes, void* stream) {
+  int rc;
+  if ((rc = check_particles(Ni, ipos)) || (rc = check_particles(Ni, iacc)) || (rc = check_particles(Nj, jpos)))
+    return rc;
+  if (flags & ~(B2_POTENTIAL | B2_EXACT)) return B2_EINVAL;
+  if (Ni == 0) return B2_OK;
+  cudaStream_t s = as_stream(stream);
+  if (Nj == 0) {
+    cudaMemsetAsync(iacc, 0, sizeof(float4) * static_cast<size_t>(Ni), s);
+    return launch_status();
+  }
+  const int nch = nchunks_for(Nj, flags);
+  if (nch == 1)
+    return launch_partials(Ni, reinterpret_cast<const float4*>(ipos), Nj, reinterpret_cast<const float4*>(jpos), eps,
+                           flags, reinterpret_cast<float4*>(iacc), s);
+  if (workspace_bytes < b2_calc_acc_workspace_bytes(Ni, Nj, flags)) return B2_ESPACE;
+  if (!aligned16(workspace)) return B2_EALIGN;
+  float4* part = static_cast<float4*>(workspace);
+  if ((rc = launch_partials(Ni, reinterpret_cast<const float4*>(ipos), Nj, reinterpret_cast<const float4*>(jpos), eps,
+                            flags, part, s)))
+    return rc;
+  return launch_update(Ni, nullptr, nullptr, reinterpret_cast<float4*>(iacc), part, nch, 0.f, 0.f, 0.f,
+                       B2_KDK_REDUCE, s);
+}
+
+int b2_kdk_update(int n, float* pos, float* vel, float* acc, const float* partials, int nchunks, float h_end,
+                  float h_begin, float dt, int phases, void* stream) {
+  int rc;
+  if (phases & ~(B2_KDK_REDUCE | B2_KDK_KICK_END | B2_KDK_KICK_DRIFT)) return B2_EINVAL;
+  if ((rc = check_particles(n, acc))) return rc;
+  if ((phases & B2_KDK_REDUCE) && ((rc = check_particles(n, partials)) || nchunks < 1)) return rc ? rc : B2_EINVAL;
+  if ((phases & (B2_KDK_KICK_END | B2_KDK_KICK_DRIFT)) && (rc = check_particles(n, vel))) return rc;
+  if ((phases & B2_KDK_KICK_DRIFT) && (rc = check_particles(n, pos))) return rc;
+  return launch_update(n, reinterpret_cast<float4*>(pos), reinterpret_cast<float4*>(vel),
+                       reinterpret_cast<float4*>(acc), reinterpret_cast<const float4*>(partials), nchunks, h_end,
+                       h_begin, dt, phases, as_stream(stream));
+}
+
+size_t b2_leapfrog_workspace_bytes(int n, int flags) {
+  const int nch = nchunks_for(n, flags & (B2_POTENTIAL | B2_EXACT));
+  return static_cast<size_t>(std::max(nch, 1)) * static_cast<size_t>(std::max(n, 0)) * sizeof(float4);
+}
+
+int b2_leapfrog(int n, float* pos, float* vel, float* acc, float eps, float dt, int nsteps, int flags,
+                void* workspace, size_t workspace_bytes, void* stream) {
+  int rc;
+  if ((rc = check_particles(n, pos)) || (rc = check_particles(n, vel)) || (rc = check_particles(n, acc))) return rc;
+  if (flags & ~(B2_POTENTIAL | B2_EXACT | B2_INIT_ACC) || nsteps < 0) return B2_EINVAL;
+  if (n == 0) return B2_OK;
+  const int fflags = flags & (B2_POTENTIAL | B2_EXACT);
+  if (workspace_bytes < b2_leapfrog_workspace_bytes(n, flags)) return B2_ESPACE;
+  if (!aligned16(workspace)) return B2_EALIGN;
+  cudaStream_t s = as_stream(stream);
+  float4* P = reinterpret_cast<float4*>(pos);
+  float4* V = reinterpret_cast<float4*>(vel);
+  float4* A = reinterpret_cast<float4*>(acc);
+  float4* part = static_cast<float4*>(workspace);
+  const int nch = nchunks_for(n, fflags);
+  const float h = 0.5f * dt;
+  if (flags & B2_INIT_ACC) {
+    if ((rc = launch_partials(n, P, n, P, eps, fflags, part, s))) return rc;
+    if ((rc = launch_update(n, P, V, A, part, nch, 0.f, 0.f, 0.f, B2_KDK_REDUCE, s))) return rc;
+  }
+  if (nsteps == 0) return B2_OK;
+  // step 0 opening kick + drift
+  if ((rc = launch_update(n, P, V, A, nullptr, nch, 0.f, h, dt, B2_KDK_KICK_DRIFT, s))) return rc;
+  for (int st = 0; st < nsteps; ++st) {
+    if ((rc = launch_partials(n, P, n, P, eps, fflags, part, s))) return rc;
+    const bool last = st + 1 == nsteps;
+    const int ph = B2_KDK_REDUCE | B2_KDK_KICK_END | (last ? 0 : B2_KDK_KICK_DRIFT);
+    if ((rc = launch_update(n, P, V, A, part, nch, h, h, dt, ph, s))) return rc;
+  }
+  return B2_OK;
+}
+
+}  // extern "C"

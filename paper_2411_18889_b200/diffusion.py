@@ -1,0 +1,128 @@
+"""7-point 3D diffusion on B200: the diffusion3d step, a device-resident time loop, grid setup.
+
+``diffusion3d`` keeps the exact name, argument order and meaning of
+``pkg/tests/fixtures/listing_diffusion.c:5``
+(``diffusion3d(nx, ny, nz, dx, dy, dz, dt, kappa, f, fn)``) with CUDA
+tensors as ``f`` / ``fn``; it runs the sm_100a marching kernel in
+``csrc/diffusion.cu``. The buffers follow the reference's
+``INDEX = k + nz*(j + ny*i)`` (listing_diffusion.c:1): a C-contiguous
+``float32[nx, ny, nz]`` tensor. Like ``ACC_CLAUSE_PRESENT(f, fn)``
+(listing_diffusion.c:10) the data must already be device-resident.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import torch
+
+from ._lib import check, load, require_cuda, stream_handle
+
+
+def _grid(t: torch.Tensor, n: int, name: str) -> None:
+    require_cuda(t, name)
+    if t.dtype != torch.float32:
+        raise TypeError(f"{name} must be float32 (listing_diffusion.c:5), got {t.dtype}")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous (INDEX = k + nz*(j + ny*i))")
+    if t.numel() < n:
+        raise ValueError(f"{name} has {t.numel()} cells, need {n}")
+
+
+def coefficients(dx: float, dy: float, dz: float, dt: float, kappa: float) -> dict[str, float]:
+    """ce, cn, ct, cc as listing_diffusion.c:6-9 (stable iff cc >= 0)."""
+    import numpy as np
+
+    f = np.float32
+    kd = f(kappa) * f(dt)
+    ce, cn, ct = kd / (f(dx) * f(dx)), kd / (f(dy) * f(dy)), kd / (f(dz) * f(dz))
+    cc = f(1.0) - (((((ce + ce) + cn) + cn) + ct) + ct)
+    return {"cc": float(cc), "ce": float(ce), "cw": float(ce), "cn": float(cn), "cs": float(cn),
+            "ct": float(ct), "cb": float(ct)}
+
+
+def diffusion3d(nx: int, ny: int, nz: int, dx: float, dy: float, dz: float, dt: float, kappa: float,
+                f: torch.Tensor, fn: torch.Tensor) -> None:
+    """One explicit step ``fn = f + kappa dt lap(f)`` with clamped boundaries (listing_diffusion.c:5-25).
+
+    Stream-ordered on the current CUDA stream; bit-identical to the reference's -O3 build.
+    """
+    n = nx * ny * nz
+    _grid(f, n, "f")
+    _grid(fn, n, "fn")
+    if f.data_ptr() == fn.data_ptr():
+        raise ValueError("f and fn must not alias (restrict, listing_diffusion.c:5)")
+    with torch.cuda.device(f.device):
+        check(load().b2_diffusion3d(nx, ny, nz, dx, dy, dz, dt, kappa, f.data_ptr(), fn.data_ptr(),
+                                    stream_handle(f.device)), "diffusion3d")
+
+
+def diffusion3d_slab(f: torch.Tensor, fn: torch.Tensor, halo_lo: torch.Tensor | None, halo_hi: torch.Tensor | None,
+                     dx: float, dy: float, dz: float, dt: float, kappa: float, i_begin: int = 0,
+                     i_end: int | None = None) -> None:
+    """Slab step for i-decomposed grids (b2_diffusion3d_slab): ``f`` is ``[nx_local, ny, nz]``;
+    ``halo_lo``/``halo_hi`` are the neighbours' edge planes or None at a global boundary."""
+    nx, ny, nz = f.shape
+    _grid(f, f.numel(), "f")
+    _grid(fn, f.numel(), "fn")
+    for h, name in ((halo_lo, "halo_lo"), (halo_hi, "halo_hi")):
+        if h is not None:
+            _grid(h, ny * nz, name)
+    ptr = lambda t: t.data_ptr() if t is not None else None  # noqa: E731
+    i_end = nx if i_end is None else i_end
+    with torch.cuda.device(f.device):
+        check(load().b2_diffusion3d_slab(nx, ny, nz, dx, dy, dz, dt, kappa, f.data_ptr(), ptr(halo_lo),
+                                         ptr(halo_hi), fn.data_ptr(), i_begin, i_end, stream_handle(f.device)),
+              "diffusion3d_slab")
+
+
+@dataclass
+class Diffusion3D:
+    """Device-resident time loop with ping-pong buffers.
+
+    ``run(n)`` advances ``n`` steps with no host synchronisation; ``field``
+    is the current solution.
+    """
+
+    f: torch.Tensor
+    dx: float
+    dy: float
+    dz: float
+    dt: float
+    kappa: float = 1.0
+    _fn: torch.Tensor = field(init=False, repr=False)
+
+    def __post_init__(self) -> None:
+        if self.f.dim() != 3:
+            raise ValueError("f must be [nx, ny, nz]")
+        _grid(self.f, self.f.numel(), "f")
+        self._fn = torch.empty_like(self.f)
+
+    @property
+    def field(self) -> torch.Tensor:
+        return self.f
+
+    def run(self, nsteps: int) -> torch.Tensor:
+        nx, ny, nz = self.f.shape
+        with torch.cuda.device(self.f.device):
+            check(load().b2_diffusion3d_run(nx, ny, nz, self.dx, self.dy, self.dz, self.dt, self.kappa,
+                                            self.f.data_ptr(), self._fn.data_ptr(), int(nsteps),
+                                            stream_handle(self.f.device)), "diffusion3d_run")
+        if nsteps % 2:
+            self.f, self._fn = self._fn, self.f
+        return self.f
+
+
+def init_grid(nx: int, ny: int, nz: int, kind: str = "uniform", seed: int = 7,
+              device: torch.device | str = "cuda") -> torch.Tensor:
+    """Synthetic initial field: U[0,1) (seeded) or a Gaussian blob.
+
+    Setup, not the hot path: generated with torch on ``device``.
+    """
+    if kind == "uniform":
+        g = torch.Generator(device=device).manual_seed(seed)
+        return torch.rand((nx, ny, nz), generator=g, dtype=torch.float32, device=device)
+    if kind == "blob":
+        axes = [(torch.arange(n, device=device, dtype=torch.float32) + 0.5) / n - 0.5 for n in (nx, ny, nz)]
+        x, y, z = torch.meshgrid(*axes, indexing="ij")
+        return torch.exp(-(x * x + y * y + z * z) / (2 * 0.05 ** 2)).contiguous()
+    raise ValueError(f"unknown grid kind {kind!r}")
