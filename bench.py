@@ -1,0 +1,534 @@
+#!/usr/bin/env python
+"""Benchmark: N-body Ginteractions/s & diffusion GLUPS on B200 vs roofline (BASELINE.json).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...        (N > 1)
+
+Prints ONE JSON line (rank 0). Headline = N-body (BASELINE configs[2] at
+N=1: N=2^20 Plummer, one KDK step = one force evaluation + the fused
+kick/drift; configs[3] for N>1: N=2^22 sharded over N GPUs with an NCCL
+position all-gather). The diffusion numbers (configs[1]'s kernel at the
+north star's 512^3 on one GPU; configs[4]'s 1024^3 slabs for N>1) ride in
+``secondary.diffusion`` with their own roofline / cpu_baseline / e2e.
+
+``--impl reference`` times the reference's OWN CPU implementation
+(oracle/_ref: the paper's listings lowered by the reference transpiler's
+fallback backend, g++ -Ofast -fopenmp) on the host cores, on bounded samples
+of the same workloads. That leg and the ``cpu_baseline`` leg are the only
+places this script touches ``oracle/``.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import os
+import pathlib
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = pathlib.Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "N-body Ginteractions/s & diffusion GLUPS at 1/2/4/8 B200 vs roofline"
+EPS = 2.0 ** -6
+DT = 2.0 ** -7
+FLOP_PER_INTERACTION = 20  # north-star convention
+BYTES_PER_CELL = 8         # one read of f, one write of fn
+
+
+def parse_args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--n", type=int, default=None, help="override particle count")
+    ap.add_argument("--grid", type=int, default=None, help="override diffusion grid edge")
+    ap.add_argument("--dsteps", type=int, default=50, help="timed diffusion steps")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-diffusion", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=8.0, help="target CPU time per baseline sample")
+    return ap.parse_args()
+
+
+# ---------------------------------------------------------------------------
+# clocks sampled during the timed region (B200_PROFILING.md recipe)
+
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    NAMES = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.file = None
+
+    def start(self):
+        try:
+            self.file = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits", "-lms", "100",
+                 "-i", str(self.index)], stdout=self.file, stderr=subprocess.DEVNULL)
+        except (OSError, FileNotFoundError):
+            self.proc = None
+        return self
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        self.file.flush()
+        rows = []
+        for line in pathlib.Path(self.file.name).read_text().splitlines():
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                rows.append((float(parts[1]), float(parts[2]), parts[5:9]))
+            except ValueError:
+                continue
+        os.unlink(self.file.name)
+        if not rows:
+            return None
+        reasons = sorted({self.NAMES[k] for _, _, r in rows for k in range(4) if r[k].lower() == "active"})
+        return {"sm_mhz": statistics.median(r[0] for r in rows), "sm_max_mhz": max(r[1] for r in rows),
+                "reasons": reasons, "samples": len(rows)}
+
+
+def measured_peaks() -> dict:
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        return json.loads(p.read_text())
+    return {"hbm_gbs": 6650.0, "_source": "fallback (B200_PROFILING.md)"}
+
+
+def ncu_traffic(kernel: str):
+    """dram bytes per launch for `kernel` from the committed ncu summary, or None."""
+    p = ROOT / "profiles" / "ncu_summary.json"
+    if not p.exists():
+        return None
+    try:
+        return json.loads(p.read_text()).get(kernel, {}).get("dram_bytes_per_launch")
+    except (ValueError, AttributeError):
+        return None
+
+
+# ---------------------------------------------------------------------------
+# CPU legs (the only users of oracle/)
+
+def _omp_env():
+    os.environ.setdefault("OMP_NUM_THREADS", str(os.cpu_count() or 1))
+    os.environ.setdefault("OMP_PROC_BIND", "close")
+
+
+def cpu_nbody_sample(pos, target_s: float):
+    """Reference fallback build (-Ofast) on a bounded i-sample against all j. Returns (Ginter/s, ni, seconds)."""
+    import numpy as np
+
+    import oracle
+
+    ref = oracle.Reference("fast")
+    n = pos.shape[0]
+    rng = np.random.default_rng(1234)
+    t0 = time.perf_counter()
+    probe = pos[rng.choice(n, 256, replace=False)]
+    ref.calc_acc(probe, pos, EPS)
+    dt0 = max(time.perf_counter() - t0, 1e-4)
+    ni = int(min(n, max(256, 256 * target_s / dt0)))
+    ni = max(64, ni // 64 * 64)
+    sample = pos[rng.choice(n, ni, replace=False)]
+    t0 = time.perf_counter()
+    ref.calc_acc(sample, pos, EPS)
+    dt = time.perf_counter() - t0
+    return ni * n / dt / 1e9, ni, dt
+
+
+def cpu_diffusion_sample(f_host, args, target_s: float):
+    import oracle
+
+    ref = oracle.Reference("fast")
+    t0 = time.perf_counter()
+    a = ref.diffusion3d(f_host, *args)
+    dt0 = max(time.perf_counter() - t0, 1e-4)
+    steps = int(max(1, min(50, target_s / dt0)))
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        a = ref.diffusion3d(a, *args)
+    dt = time.perf_counter() - t0
+    return f_host.size * steps / dt / 1e9, steps, dt
+
+
+def cpu_info() -> str:
+    try:
+        for line in pathlib.Path("/proc/cpuinfo").read_text().splitlines():
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+# ---------------------------------------------------------------------------
+# reference arm
+
+def run_reference(args, rank: int, world: int):
+    if rank != 0:
+        return None
+    _omp_env()
+    import numpy as np
+
+    from paper_2411_18889_b200.nbody import plummer_numpy
+
+    n = args.n or (1 << 20)
+    pos, _ = plummer_numpy(n, 42)
+    per_step = max(1.0, args.cpu_seconds / 2)
+    for _ in range(args.warmup):
+        cpu_nbody_sample(pos, per_step / 4)
+    vals, nis = [], []
+    t_all = 0.0
+    for _ in range(args.steps):
+        v, ni, dt = cpu_nbody_sample(pos, per_step)
+        vals.append(v)
+        nis.append(ni)
+        t_all += dt
+    value = statistics.mean(vals)
+    cores = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
+    out = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "Ginteractions/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t_all / args.steps,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic Plummer sphere (seed 42)",
+        "config": {"workload": f"nbody N={n} Plummer FP32 force evaluation (reference CPU: sampled i x all j)",
+                   "n": n, "sample_i": nis[-1]},
+        "cpu_baseline": {"value": value, "unit": "Ginteractions/s", "cores": cores, "kind": "reference",
+                         "sample": f"{nis[-1]} random i x {n} j per step, libref_fast (g++ -Ofast -fopenmp), "
+                                   f"{cpu_info()}"},
+        "e2e": {"value": value, "unit": "Ginteractions/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    if not args.no_diffusion:
+        g = args.grid or 512
+        f = np.random.default_rng(7).random((g, g, g), dtype=np.float32)
+        dx = 1.0 / g
+        dargs = (dx, dx, dx, 0.1 * dx * dx, 1.0)
+        v, steps, dt = cpu_diffusion_sample(f, dargs, args.cpu_seconds)
+        out["secondary"] = {"diffusion": {
+            "metric": "diffusion GLUPS", "value": v, "unit": "GLUPS",
+            "config": {"workload": f"diffusion3d {g}^3 FP32, {steps} steps (reference CPU)"},
+            "cpu_baseline": {"value": v, "unit": "GLUPS", "cores": cores, "kind": "reference",
+                             "sample": f"{steps} steps of {g}^3, libref_fast"}}}
+    return out
+
+
+# ---------------------------------------------------------------------------
+# our arm
+
+def run_ours(args, rank: int, world: int, local_rank: int):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_2411_18889_b200 as b2
+    from paper_2411_18889_b200 import _lib
+    from paper_2411_18889_b200.distributed import ShardedLeapfrog, SlabDiffusion
+
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    lib = b2.load()
+    peaks = measured_peaks()
+    stream = torch.cuda.current_stream(dev)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
+
+    # FP32 roofline denominator, measured live on this GPU (MEASURED_PEAKS.json has no FP32 figure)
+    probe = ctypes.CDLL(str(ROOT / "paper_2411_18889_b200" / "lib" / "libsolomon_probe.so"))
+    probe.solomon_probe_fp32_tflops.restype = ctypes.c_double
+    fp32_peak = probe.solomon_probe_fp32_tflops(5)
+
+    # ---------------- N-body ----------------
+    n = args.n or ((1 << 20) if world == 1 else (1 << 22))
+    pos_np, vel_np = b2.plummer_numpy(n, 42)
+    if world == 1:
+        pos = torch.from_numpy(pos_np).to(dev)
+        vel = torch.from_numpy(vel_np).to(dev)
+        nch = lib.b2_calc_acc_nchunks(n, 0)
+        part = torch.empty((nch * n, 4), dtype=torch.float32, device=dev)
+        acc = torch.empty_like(pos)
+        h = 0.5 * DT
+        sh = _lib.stream_handle(dev)
+
+        def force():
+            _lib.check(lib.b2_calc_acc_partials(n, pos.data_ptr(), n, pos.data_ptr(), EPS, 0, part.data_ptr(), sh),
+                       "partials")
+
+        def update(phases):
+            _lib.check(lib.b2_kdk_update(n, pos.data_ptr(), vel.data_ptr(), acc.data_ptr(), part.data_ptr(), nch,
+                                         h, h, DT, phases, sh), "update")
+
+        force()
+        update(_lib.B2_KDK_REDUCE)
+        update(_lib.B2_KDK_KICK_DRIFT)
+        steady = _lib.B2_KDK_REDUCE | _lib.B2_KDK_KICK_END | _lib.B2_KDK_KICK_DRIFT
+
+        def step(evs):
+            evs[0].record(stream)
+            force()
+            evs[1].record(stream)
+            update(steady)
+            evs[2].record(stream)
+
+        n_local = n
+        launches_per_step = 2
+        parallelism = "single GPU"
+    else:
+        plan_lo = rank * (n // world)
+        sim = ShardedLeapfrog(torch.from_numpy(pos_np[plan_lo:plan_lo + n // world]).to(dev),
+                              torch.from_numpy(vel_np[plan_lo:plan_lo + n // world]).to(dev), EPS, DT)
+        sim.step(1, close=False)
+        n_local = n // world
+
+        def step(evs):
+            evs[0].record(stream)
+            sim.gather()
+            evs[3].record(stream)
+            sim.k.partials(sim.pos, sim.pos_all, sim.eps, sim.part)
+            evs[1].record(stream)
+            hh = 0.5 * DT
+            sim.k.update(sim.pos, sim.vel, sim.acc, sim.part, sim.nch, hh, hh, DT,
+                         _lib.B2_KDK_REDUCE | _lib.B2_KDK_KICK_END | _lib.B2_KDK_KICK_DRIFT)
+            evs[2].record(stream)
+
+        launches_per_step = 2
+        parallelism = f"i-shard x{world}, NCCL all_gather_into_tensor of positions per step"
+
+    mk = lambda: [torch.cuda.Event(enable_timing=True) for _ in range(4)]  # noqa: E731
+    for _ in range(args.warmup):
+        flush.zero_()
+        step(mk())
+    torch.cuda.synchronize(dev)
+    barrier()
+    clocks = ClockSampler(local_rank).start() if rank == 0 else None
+    torch.cuda.synchronize(dev)
+    barrier()
+    events = []
+    for _ in range(args.steps):
+        flush.zero_()  # L2 flush between timed steps (outside the events)
+        evs = mk()
+        step(evs)
+        events.append(evs)
+    torch.cuda.synchronize(dev)
+    barrier()
+    clock_rec = clocks.stop() if clocks else None
+    step_ms = [e[0].elapsed_time(e[2]) for e in events]
+    force_ms = [(e[3] if world > 1 else e[0]).elapsed_time(e[1]) for e in events]
+    total_ms = max_over_ranks(sum(step_ms))
+    force_avg = max_over_ranks(statistics.mean(force_ms))
+    gather_ms = max_over_ranks(statistics.mean(e[0].elapsed_time(e[3]) for e in events)) if world > 1 else 0.0
+    interactions = float(n) * float(n)
+    value = interactions * args.steps / (total_ms * 1e-3) / 1e9
+    achieved_tf = FLOP_PER_INTERACTION * float(n_local) * float(n) / (force_avg * 1e-3) / 1e12
+
+    result = {
+        "metric": METRIC, "value": value, "unit": "Ginteractions/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic: Plummer sphere (seed 42, FP64 -> FP32 on host); diffusion grid U[0,1) (seed 7)",
+        "config": {
+            "workload": (f"nbody N={n} Plummer FP32, one KDK leapfrog step per step "
+                         f"(force evaluation of N^2 interactions + fused reduce/kick/drift)"),
+            "n": n, "eps": EPS, "dt": DT, "jchunks": int(lib.b2_calc_acc_nchunks(n, 0)),
+            "parallelism": parallelism,
+            "l2": "flushed between timed steps (512 MiB memset, outside the step events)",
+        },
+        "roofline": {
+            "bound": "fp32", "kernel": "k_force_fast", "achieved": achieved_tf, "peak": fp32_peak,
+            "unit": "TFLOP/s", "frac": achieved_tf / fp32_peak if fp32_peak > 0 else None,
+            "traffic": ncu_traffic("k_force_fast"),
+            "flop_per_interaction": FLOP_PER_INTERACTION,
+            "peak_source": "measured live: packed-FFMA2 throughput probe on this GPU "
+                           "(MEASURED_PEAKS.json has no FP32 figure; nominal 148x128x2x1.965 GHz = 74.4)",
+            "force_ms": force_avg, "allgather_ms": gather_ms,
+        },
+        "gpu_launches": launches_per_step * args.steps,
+        "clocks": clock_rec,
+    }
+
+    # e2e through the reference-facing drop-in with HOST (pinned) buffers
+    if world == 1:
+        hpos = torch.from_numpy(pos_np).pin_memory()
+        hacc = torch.empty_like(hpos).pin_memory()
+        P = ctypes.c_void_p
+        lib.calc_acc(n, P(hpos.data_ptr()), P(hacc.data_ptr()), n, P(hpos.data_ptr()), EPS)  # warm the arena
+        t0 = time.perf_counter()
+        k_e2e = max(1, min(args.steps, 3))
+        for _ in range(k_e2e):
+            lib.calc_acc(n, P(hpos.data_ptr()), P(hacc.data_ptr()), n, P(hpos.data_ptr()), EPS)
+        t_e2e = (time.perf_counter() - t0) / k_e2e
+        _lib.check(lib.b2_last_error(), "calc_acc drop-in")
+        result["e2e"] = {"value": interactions / t_e2e / 1e9, "unit": "Ginteractions/s",
+                         "h2d_bytes_per_step": 16 * n, "d2h_bytes_per_step": 16 * n,
+                         "api": "calc_acc(Ni, ipos, iacc, Nj, jpos, eps) C drop-in, pinned host buffers "
+                                "(ipos == jpos staged once), synchronous", "steps": k_e2e}
+        del hpos, hacc
+    else:
+        result["e2e"] = None
+
+    # ---------------- diffusion ----------------
+    if not args.no_diffusion:
+        result["secondary"] = {"diffusion": run_diffusion(args, rank, world, dev, stream, peaks, barrier,
+                                                          max_over_ranks, flush)}
+
+    # ---------------- CPU baseline (rank 0, N=1) ----------------
+    if world == 1 and rank == 0 and not args.no_cpu_baseline:
+        _omp_env()
+        cores = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
+        try:
+            v, ni, dt = cpu_nbody_sample(pos_np, args.cpu_seconds)
+            result["cpu_baseline"] = {"value": v, "unit": "Ginteractions/s", "cores": cores, "kind": "reference",
+                                      "sample": f"{ni} random i x {n} j (one sampled force evaluation, {dt:.1f} s), "
+                                                f"oracle/_ref libref_fast (reference listing via its fallback "
+                                                f"lowering, g++ -Ofast -fopenmp), {cpu_info()}"}
+        except FileNotFoundError as e:
+            result["cpu_baseline"] = {"value": None, "unavailable": str(e)}
+    return result
+
+
+def run_diffusion(args, rank, world, dev, stream, peaks, barrier, max_over_ranks, flush):
+    import torch
+
+    import paper_2411_18889_b200 as b2
+    from paper_2411_18889_b200.distributed import SlabDiffusion
+
+    lib = b2.load()
+    g = args.grid or (512 if world == 1 else 1024)
+    dx = 1.0 / g
+    dargs = (dx, dx, dx, 0.1 * dx * dx, 1.0)
+    if world == 1:
+        f = b2.init_grid(g, g, g, seed=7, device=dev)
+        fn = torch.empty_like(f)
+        bufs = [f, fn]
+
+        def dstep(i):
+            a, b = bufs[i % 2], bufs[(i + 1) % 2]
+            b2.diffusion3d(g, g, g, *dargs, a, b)
+
+        launches = 1
+        nxl = g
+    else:
+        nxl = g // world
+        gen = torch.Generator(device=dev).manual_seed(7 + rank)
+        f_local = torch.rand((nxl, g, g), generator=gen, dtype=torch.float32, device=dev)
+        sim = SlabDiffusion(f_local, *dargs)
+
+        def dstep(i):
+            sim.step(1)
+
+        launches = sim.launches_per_step()
+    for i in range(5):
+        dstep(i)
+    torch.cuda.synchronize(dev)
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for i in range(args.dsteps):  # back to back: inputs (2 x field) exceed L2, no flush needed
+        dstep(i)
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    barrier()
+    total_ms = max_over_ranks(e0.elapsed_time(e1))
+    step_ms = total_ms / args.dsteps
+    cells = float(g) ** 3
+    glups = cells * args.dsteps / (total_ms * 1e-3) / 1e9
+    kernel_ms = step_ms  # one launch per step at N=1: average launch duration over the timed region
+    achieved = BYTES_PER_CELL * float(nxl) * g * g / (kernel_ms * 1e-3) / 1e9
+    out = {
+        "metric": "diffusion GLUPS", "value": glups, "unit": "GLUPS", "ms_per_step": step_ms,
+        "steps": args.dsteps, "warmup": 5, "dtype": "f32",
+        "config": {"workload": f"diffusion3d {g}^3 FP32 7-point step" + (" (single GPU)" if world == 1 else
+                                                                          f", i-slabs x{world} + NCCL halo"),
+                   "grid": [g, g, g], "dt_over_dx2": 0.1,
+                   "l2": "inputs (2 x {:.0f} MiB per GPU) larger than L2; no flush".format(4 * nxl * g * g / 2**20)},
+        "roofline": {"bound": "hbm", "kernel": "k_diffusion_march", "achieved": achieved,
+                     "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"],
+                     "traffic": ncu_traffic("k_diffusion_march"), "bytes_per_cell": BYTES_PER_CELL,
+                     "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "_source" not in peaks else peaks["_source"]},
+        "gpu_launches": launches * args.dsteps,
+    }
+    if world == 1:
+        host_f = f.cpu().pin_memory()
+        host_fn = torch.empty_like(host_f).pin_memory()
+        P = ctypes.c_void_p
+        lib.diffusion3d(g, g, g, *dargs, P(host_f.data_ptr()), P(host_fn.data_ptr()))
+        k = 3
+        t0 = time.perf_counter()
+        for _ in range(k):
+            lib.diffusion3d(g, g, g, *dargs, P(host_f.data_ptr()), P(host_fn.data_ptr()))
+        t = (time.perf_counter() - t0) / k
+        out["e2e"] = {"value": cells / t / 1e9, "unit": "GLUPS", "h2d_bytes_per_step": int(4 * cells),
+                      "d2h_bytes_per_step": int(4 * cells),
+                      "api": "diffusion3d(nx,...,f,fn) C drop-in, pinned host buffers, synchronous"}
+        if rank == 0 and not args.no_cpu_baseline:
+            _omp_env()
+            try:
+                v, steps, dt = cpu_diffusion_sample(host_f.numpy(), dargs, args.cpu_seconds / 2)
+                out["cpu_baseline"] = {"value": v, "unit": "GLUPS",
+                                       "cores": int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1)),
+                                       "kind": "reference",
+                                       "sample": f"{steps} steps of {g}^3 ({dt:.1f} s), oracle/_ref libref_fast"}
+            except FileNotFoundError as e:
+                out["cpu_baseline"] = {"value": None, "unavailable": str(e)}
+        del host_f, host_fn
+    return out
+
+
+def main():
+    args = parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.gpus != world and world > 1:
+        print(f"warning: --gpus {args.gpus} but WORLD_SIZE {world}", file=sys.stderr)
+    if args.impl == "reference":
+        out = run_reference(args, rank, world)
+        if out is not None:
+            print(json.dumps(out), flush=True)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    out = run_ours(args, rank, world, local_rank)
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -78,8 +78,28 @@ class Restatement(_Base):
         L.oracle_diffusion3d.argtypes = [ctypes.c_int] * 3 + [ctypes.c_float] * 5 + [_f32p, _f32p]
         L.oracle_leapfrog.argtypes = [ctypes.c_int, _f32p, _f32p, _f32p, ctypes.c_float, ctypes.c_float,
                                       ctypes.c_int, ctypes.c_int]
+        L.oracle_calc_acc_partials.argtypes = [ctypes.c_int, _f32p, ctypes.c_int, _f32p, ctypes.c_float,
+                                               ctypes.c_int, ctypes.c_int, _f32p]
+        L.oracle_kdk_update.argtypes = [ctypes.c_int, _f32p, _f32p, _f32p, _f32p, ctypes.c_int, ctypes.c_float,
+                                        ctypes.c_float, ctypes.c_float, ctypes.c_int]
         self._calc_acc = L.oracle_calc_acc
         self._diffusion3d = L.oracle_diffusion3d
+
+    def calc_acc_partials(self, ipos, jpos, eps, chunk, potential=False, out=None):
+        ipos = np.ascontiguousarray(ipos, dtype=np.float32)
+        jpos = np.ascontiguousarray(jpos, dtype=np.float32)
+        nch = (jpos.shape[0] + chunk - 1) // chunk
+        if out is None:
+            out = np.empty((nch * ipos.shape[0], 4), np.float32)
+        self.lib.oracle_calc_acc_partials(ipos.shape[0], _ptr(ipos), jpos.shape[0], _ptr(jpos), ctypes.c_float(eps),
+                                          int(potential), int(chunk), _ptr(out))
+        return out
+
+    def kdk_update(self, pos, vel, acc, partials, nchunks, h_end, h_begin, dt, phases):
+        """In place on float32 C-contiguous arrays (None allowed where the phase does not use it)."""
+        p = lambda a: _ptr(a) if a is not None else None  # noqa: E731
+        self.lib.oracle_kdk_update(acc.shape[0], p(pos), p(vel), _ptr(acc), p(partials), int(nchunks),
+                                   ctypes.c_float(h_end), ctypes.c_float(h_begin), ctypes.c_float(dt), int(phases))
 
     def leapfrog(self, pos, vel, eps, dt, nsteps, potential=False):
         """Returns (pos, vel, acc) after ``nsteps`` KDK steps (spec: solomon_oracle.c)."""

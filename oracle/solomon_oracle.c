@@ -133,3 +133,42 @@ void oracle_leapfrog(int n, float *pos, float *vel, float *acc, float eps, float
     oracle_kick(n, vel, acc, h);
   }
 }
+
+/* ---------------------------------------------------------------------------
+ * Chunked force + fused update: restates the STRUCTURE of the fast GPU path
+ * (csrc/nbody.cu) with the reference's per-pair arithmetic, so the multi-rank
+ * exchange logic (paper_2411_18889_b200/distributed.py) can be checked on CPU.
+ * partials[c*Ni + i] = sum over j in chunk c (sequential from 0).
+ */
+void oracle_calc_acc_partials(int Ni, const float *ipos, int Nj, const float *jpos, float eps, int potential,
+                              int chunk, float *partials) {
+  const int nch = (Nj + chunk - 1) / chunk;
+  for (int c = 0; c < nch; c++) {
+    const int j0 = c * chunk;
+    const int cnt = (Nj - j0) < chunk ? (Nj - j0) : chunk;
+    oracle_calc_acc(Ni, ipos, partials + 4 * (size_t)c * Ni, cnt, jpos + 4 * (size_t)j0, eps, potential);
+  }
+}
+
+/* Phases as b2_kdk_update (include/solomon_b200.h): 1 reduce, 2 closing kick, 4 opening kick + drift. */
+void oracle_kdk_update(int n, float *pos, float *vel, float *acc, const float *partials, int nchunks, float h_end,
+                       float h_begin, float dt, int phases) {
+#pragma omp parallel for schedule(static)
+  for (int i = 0; i < n; i++) {
+    float a[4];
+    if (phases & 1) {
+      for (int d = 0; d < 4; d++) a[d] = partials[4 * (size_t)i + d];
+      for (int c = 1; c < nchunks; c++)
+        for (int d = 0; d < 4; d++) a[d] = a[d] + partials[4 * ((size_t)c * n + i) + d];
+      for (int d = 0; d < 4; d++) acc[4 * (size_t)i + d] = a[d];
+    } else {
+      for (int d = 0; d < 4; d++) a[d] = acc[4 * (size_t)i + d];
+    }
+    if (phases & 2)
+      for (int d = 0; d < 3; d++) vel[4 * (size_t)i + d] = fmaf(a[d], h_end, vel[4 * (size_t)i + d]);
+    if (phases & 4) {
+      for (int d = 0; d < 3; d++) vel[4 * (size_t)i + d] = fmaf(a[d], h_begin, vel[4 * (size_t)i + d]);
+      for (int d = 0; d < 3; d++) pos[4 * (size_t)i + d] = fmaf(vel[4 * (size_t)i + d], dt, pos[4 * (size_t)i + d]);
+    }
+  }
+}

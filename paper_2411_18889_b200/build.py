@@ -19,6 +19,7 @@ ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB_DIR = PKG / "lib"
 LIB = LIB_DIR / "libsolomon_b200.so"
+PROBE = LIB_DIR / "libsolomon_probe.so"
 SOURCES = ["nbody.cu", "diffusion.cu", "dropin.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
@@ -34,7 +35,9 @@ def needs_build() -> bool:
     if not LIB.exists():
         return True
     t = LIB.stat().st_mtime
-    deps = [CSRC / s for s in SOURCES] + list(CSRC.glob("*.cuh")) + [ROOT / "include" / "solomon_b200.h"]
+    if not PROBE.exists():
+        return True
+    deps = [CSRC / s for s in SOURCES] + [CSRC / "probe.cu"] + list(CSRC.glob("*.cuh")) + [ROOT / "include" / "solomon_b200.h"]
     return any(d.stat().st_mtime > t for d in deps if d.exists())
 
 
@@ -42,6 +45,8 @@ def build(force: bool = False, verbose: bool = False) -> pathlib.Path:
     if not force and not needs_build():
         return LIB
     LIB_DIR.mkdir(exist_ok=True)
+    subprocess.run([nvcc(), *ARCH, "-O3", "-lineinfo", "-shared", "-Xcompiler", "-fPIC",
+                    str(CSRC / "probe.cu"), "-o", str(PROBE)], check=True)
     cmd = [nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler", "-fPIC",
            "-Xcompiler", "-fno-fast-math",
            "-DSOLOMON_B200_BUILD", f"-I{ROOT / 'include'}", f"-I{CSRC}",

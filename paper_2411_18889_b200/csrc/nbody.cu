@@ -25,12 +25,12 @@
 #include <algorithm>
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 
 #include "common.cuh"
 
 namespace b2 {
 
-constexpr int kIPT = 8;            // i-particles per thread (4 packed pairs)
 constexpr int kChunkAlign = 256;   // j-chunk sizes are multiples of this
 constexpr int kTargetChunks = 64;  // j-chunks per force evaluation (fast path)
 
@@ -43,10 +43,78 @@ __device__ __forceinline__ float rsqrt_approx(float x) {
 // ---------------------------------------------------------------------------
 // K1 fast: packed-FP32 tile kernel.
 // grid.x = n_itiles * nchunks; block = BLOCK threads; out = partials[c][Ni].
-template <int BLOCK, bool POT>
-__global__ void __launch_bounds__(BLOCK, (BLOCK >= 256 ? 2 : 8))
+// One j against the thread's P = IPT/2 packed i-pairs, written stage by stage
+// across the pairs (breadth-first) so every dependent FP32 op has P-1
+// independent ones in front of it -- the fixed-latency FFMA2 chain of
+// listing_nbody.c:14 otherwise leaves the FMA pipe idle (ncu "stall wait").
+template <int P, bool POT>
+__device__ __forceinline__ void interact_bf(const float2 X, const float2 Y, const float2 Z, const float2 M,
+                                            const float2 (&nx)[P], const float2 (&ny)[P], const float2 (&nz)[P],
+                                            const float2 e2, float2 (&ax)[P], float2 (&ay)[P], float2 (&az)[P],
+                                            float2 (&ap)[P]) {
+  float2 rx[P], ry[P], rz[P], r2[P], w[P];
+#pragma unroll
+  for (int p = 0; p < P; ++p) rx[p] = __fadd2_rn(X, nx[p]);
+#pragma unroll
+  for (int p = 0; p < P; ++p) ry[p] = __fadd2_rn(Y, ny[p]);
+#pragma unroll
+  for (int p = 0; p < P; ++p) rz[p] = __fadd2_rn(Z, nz[p]);
+#pragma unroll
+  for (int p = 0; p < P; ++p) r2[p] = __ffma2_rn(rx[p], rx[p], e2);
+#pragma unroll
+  for (int p = 0; p < P; ++p) r2[p] = __ffma2_rn(ry[p], ry[p], r2[p]);
+#pragma unroll
+  for (int p = 0; p < P; ++p) r2[p] = __ffma2_rn(rz[p], rz[p], r2[p]);
+#pragma unroll
+  for (int p = 0; p < P; ++p) w[p] = make_float2(rsqrt_approx(r2[p].x), rsqrt_approx(r2[p].y));
+  float2 w2[P];
+#pragma unroll
+  for (int p = 0; p < P; ++p) w2[p] = __fmul2_rn(w[p], w[p]);
+#pragma unroll
+  for (int p = 0; p < P; ++p) w[p] = __fmul2_rn(w[p], w2[p]);
+#pragma unroll
+  for (int p = 0; p < P; ++p) w[p] = __fmul2_rn(w[p], M);
+#pragma unroll
+  for (int p = 0; p < P; ++p) ax[p] = __ffma2_rn(rx[p], w[p], ax[p]);
+#pragma unroll
+  for (int p = 0; p < P; ++p) ay[p] = __ffma2_rn(ry[p], w[p], ay[p]);
+#pragma unroll
+  for (int p = 0; p < P; ++p) az[p] = __ffma2_rn(rz[p], w[p], az[p]);
+  if (POT) {
+#pragma unroll
+    for (int p = 0; p < P; ++p) ap[p] = __ffma2_rn(r2[p], w[p], ap[p]);
+  }
+}
+
+// Depth-first form (one pair at a time), kept as a tuning variant.
+template <int P, bool POT>
+__device__ __forceinline__ void interact_df(const float2 X, const float2 Y, const float2 Z, const float2 M,
+                                            const float2 (&nx)[P], const float2 (&ny)[P], const float2 (&nz)[P],
+                                            const float2 e2, float2 (&ax)[P], float2 (&ay)[P], float2 (&az)[P],
+                                            float2 (&ap)[P]) {
+#pragma unroll
+  for (int p = 0; p < P; ++p) {
+    const float2 rx = __fadd2_rn(X, nx[p]);
+    const float2 ry = __fadd2_rn(Y, ny[p]);
+    const float2 rz = __fadd2_rn(Z, nz[p]);
+    float2 r2 = __ffma2_rn(rx, rx, e2);
+    r2 = __ffma2_rn(ry, ry, r2);
+    r2 = __ffma2_rn(rz, rz, r2);
+    float2 w = make_float2(rsqrt_approx(r2.x), rsqrt_approx(r2.y));
+    w = __fmul2_rn(w, __fmul2_rn(w, w));
+    w = __fmul2_rn(w, M);
+    ax[p] = __ffma2_rn(rx, w, ax[p]);
+    ay[p] = __ffma2_rn(ry, w, ay[p]);
+    az[p] = __ffma2_rn(rz, w, az[p]);
+    if (POT) ap[p] = __ffma2_rn(r2, w, ap[p]);
+  }
+}
+
+template <int BLOCK, int kIPT, int MINB, int UNR, int SCHED, bool POT>
+__global__ void __launch_bounds__(BLOCK, MINB)
     k_force_fast(const float4* __restrict__ ipos, int Ni, const float4* __restrict__ jpos, int Nj,
                  int jchunk, int n_itiles, float eps2, float4* __restrict__ out) {
+  constexpr int P = kIPT / 2;
   __shared__ float4 sj[2][2 * BLOCK];
 
   const int tid = threadIdx.x;
@@ -54,10 +122,10 @@ __global__ void __launch_bounds__(BLOCK, (BLOCK >= 256 ? 2 : 8))
   const int chunk = blockIdx.x / n_itiles;
   const int ibase = itile * (BLOCK * kIPT) + tid;
 
-  float2 nx[kIPT / 2], ny[kIPT / 2], nz[kIPT / 2];
-  float2 ax[kIPT / 2], ay[kIPT / 2], az[kIPT / 2], ap[kIPT / 2];
+  float2 nx[P], ny[P], nz[P];
+  float2 ax[P], ay[P], az[P], ap[P];
 #pragma unroll
-  for (int p = 0; p < kIPT / 2; ++p) {
+  for (int p = 0; p < P; ++p) {
     const int ia = min(ibase + (2 * p) * BLOCK, Ni - 1);
     const int ib = min(ibase + (2 * p + 1) * BLOCK, Ni - 1);
     const float4 a = __ldg(ipos + ia), b = __ldg(ipos + ib);
@@ -94,7 +162,7 @@ __global__ void __launch_bounds__(BLOCK, (BLOCK >= 256 ? 2 : 8))
     if (more) next = fetch(t + 1);
 
     const float4* __restrict__ s = sj[buf];
-#pragma unroll 4
+#pragma unroll UNR
     for (int jj = 0; jj < BLOCK; ++jj) {
       const float4 A = s[2 * jj + 0];
       const float4 B = s[2 * jj + 1];
@@ -102,22 +170,10 @@ __global__ void __launch_bounds__(BLOCK, (BLOCK >= 256 ? 2 : 8))
       const float2 Y = make_float2(A.z, A.w);
       const float2 Z = make_float2(B.x, B.y);
       const float2 M = make_float2(B.z, B.w);
-#pragma unroll
-      for (int p = 0; p < kIPT / 2; ++p) {
-        const float2 rx = __fadd2_rn(X, nx[p]);
-        const float2 ry = __fadd2_rn(Y, ny[p]);
-        const float2 rz = __fadd2_rn(Z, nz[p]);
-        float2 r2 = __ffma2_rn(rx, rx, e2);
-        r2 = __ffma2_rn(ry, ry, r2);
-        r2 = __ffma2_rn(rz, rz, r2);
-        float2 w = make_float2(rsqrt_approx(r2.x), rsqrt_approx(r2.y));
-        w = __fmul2_rn(w, __fmul2_rn(w, w));
-        w = __fmul2_rn(w, M);
-        ax[p] = __ffma2_rn(rx, w, ax[p]);
-        ay[p] = __ffma2_rn(ry, w, ay[p]);
-        az[p] = __ffma2_rn(rz, w, az[p]);
-        if (POT) ap[p] = __ffma2_rn(r2, w, ap[p]);
-      }
+      if (SCHED == 1)
+        interact_bf<P, POT>(X, Y, Z, M, nx, ny, nz, e2, ax, ay, az, ap);
+      else
+        interact_df<P, POT>(X, Y, Z, M, nx, ny, nz, e2, ax, ay, az, ap);
     }
     if (more) stash(buf ^ 1, next);
     __syncthreads();
@@ -125,7 +181,7 @@ __global__ void __launch_bounds__(BLOCK, (BLOCK >= 256 ? 2 : 8))
 
   float4* __restrict__ o = out + static_cast<size_t>(chunk) * Ni;
 #pragma unroll
-  for (int p = 0; p < kIPT / 2; ++p) {
+  for (int p = 0; p < P; ++p) {
     const int ia = ibase + (2 * p) * BLOCK;
     const int ib = ibase + (2 * p + 1) * BLOCK;
     if (ia < Ni) o[ia] = make_float4(ax[p].x, ay[p].x, az[p].x, POT ? ap[p].x : 0.f);
@@ -226,6 +282,36 @@ static int nchunks_for(int Nj, int flags) {
   return (Nj + c - 1) / c;
 }
 
+// Launch variants of the fast kernel: {threads, i per thread, min CTAs/SM, j unroll}.
+struct ForceVariant {
+  int block, ipt;
+  void (*fn[2])(const float4*, int, const float4*, int, int, int, float, float4*);
+};
+#define B2_FV(B, I, M, U, S) \
+  { B, I, { k_force_fast<B, I, M, U, S, false>, k_force_fast<B, I, M, U, S, true> } }
+static const ForceVariant kVariants[] = {
+    B2_FV(256, 8, 2, 4, 1),  // 0: default for large N
+    B2_FV(64, 8, 8, 4, 1),   // 1: small N (more CTAs)
+    B2_FV(256, 8, 2, 4, 0),  // 2: depth-first schedule (round-1 baseline)
+    B2_FV(256, 4, 4, 8, 0),  // 3
+    B2_FV(256, 4, 4, 8, 1),  // 4
+    B2_FV(256, 8, 2, 2, 1),  // 5
+    B2_FV(128, 8, 4, 4, 1),  // 6
+    B2_FV(256, 4, 3, 4, 1),  // 7
+    B2_FV(256, 12, 1, 2, 1), // 8
+    B2_FV(256, 4, 4, 4, 1),  // 9
+};
+#undef B2_FV
+
+static int large_variant() {
+  static int v = [] {
+    const char* e = std::getenv("SOLOMON_NBODY_VARIANT");  // tuning knob (bench sweeps)
+    int x = e ? std::atoi(e) : 0;
+    return (x >= 0 && x < static_cast<int>(sizeof(kVariants) / sizeof(kVariants[0]))) ? x : 0;
+  }();
+  return v;
+}
+
 static int launch_partials(int Ni, const float4* ipos, int Nj, const float4* jpos, float eps, int flags,
                            float4* out, cudaStream_t s) {
   const float eps2 = eps * eps;  // listing_nbody.c:5
@@ -241,23 +327,12 @@ static int launch_partials(int Ni, const float4* ipos, int Nj, const float4* jpo
   const int jchunk = chunk_size(Nj, flags);
   const int nch = nchunks_for(Nj, flags);
   // Small i-sets use 64-thread CTAs so that the (i-tile, j-chunk) grid still
-  // covers the 148 SMs; large ones use 256-thread CTAs (2 per SM).
-  const bool small = static_cast<long long>((Ni + 256 * kIPT - 1) / (256 * kIPT)) * nch < 8LL * device_info().sms;
-  if (small) {
-    const int nit = (Ni + 64 * kIPT - 1) / (64 * kIPT);
-    const dim3 grid(nit * nch);
-    if (pot)
-      k_force_fast<64, true><<<grid, 64, 0, s>>>(ipos, Ni, jpos, Nj, jchunk, nit, eps2, out);
-    else
-      k_force_fast<64, false><<<grid, 64, 0, s>>>(ipos, Ni, jpos, Nj, jchunk, nit, eps2, out);
-  } else {
-    const int nit = (Ni + 256 * kIPT - 1) / (256 * kIPT);
-    const dim3 grid(nit * nch);
-    if (pot)
-      k_force_fast<256, true><<<grid, 256, 0, s>>>(ipos, Ni, jpos, Nj, jchunk, nit, eps2, out);
-    else
-      k_force_fast<256, false><<<grid, 256, 0, s>>>(ipos, Ni, jpos, Nj, jchunk, nit, eps2, out);
-  }
+  // covers the 148 SMs; large ones use the tuned variant.
+  const ForceVariant* v = &kVariants[large_variant()];
+  const long long tiles = (Ni + v->block * v->ipt - 1) / (v->block * v->ipt);
+  if (tiles * nch < 8LL * device_info().sms) v = &kVariants[1];
+  const int nit = (Ni + v->block * v->ipt - 1) / (v->block * v->ipt);
+  v->fn[pot ? 1 : 0]<<<nit * nch, v->block, 0, s>>>(ipos, Ni, jpos, Nj, jchunk, nit, eps2, out);
   return launch_status();
 }
 

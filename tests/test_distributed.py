@@ -1,0 +1,158 @@
+"""CPU, world_size 2-3 over gloo: the multi-GPU partitioning logic.
+
+The compute backend is injected with the oracle (CPU) so the exchange logic --
+shard offsets, in-place position all-gather, halo planes, global-boundary
+clamps, interior/boundary split -- is exercised without a GPU. The property
+checked is the one the design promises: sharded == unsharded, bit for bit.
+"""
+from __future__ import annotations
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+
+class OracleNBodyKernels:
+    """CPU stand-in for distributed.CudaNBodyKernels (same chunked structure)."""
+
+    def __init__(self, chunk: int):
+        import oracle
+
+        self.o = oracle.Restatement()
+        self.chunk = chunk
+
+    def nchunks(self, nj):
+        return (nj + self.chunk - 1) // self.chunk
+
+    def partials(self, ipos, jpos, eps, out):
+        self.o.calc_acc_partials(ipos.numpy(), jpos.numpy(), eps, self.chunk, out=out.numpy())
+
+    def update(self, pos, vel, acc, partials, nchunks, h_end, h_begin, dt, phases):
+        n = lambda t: t.numpy() if t is not None else None  # noqa: E731
+        self.o.kdk_update(n(pos), n(vel), acc.numpy(), n(partials), nchunks, h_end, h_begin, dt, phases)
+
+
+class OracleSlabKernels:
+    """CPU stand-in for distributed.CudaSlabKernels: the oracle on the halo-extended slab."""
+
+    def __init__(self, *args):
+        import oracle
+
+        self.o = oracle.Restatement()
+        self.args = args
+
+    def slab(self, f, fn, halo_lo, halo_hi, i_begin, i_end):
+        a = f.numpy()
+        lo = halo_lo.numpy() if halo_lo is not None else a[0]  # absent halo == clamp IMAX(i-1,0)
+        hi = halo_hi.numpy() if halo_hi is not None else a[-1]
+        ext = np.concatenate([lo[None], a, hi[None]], axis=0)
+        out = self.o.diffusion3d(ext, *self.args)
+        fn.numpy()[i_begin:i_end] = out[1 + i_begin:1 + i_end]
+
+
+def _free_port() -> int:
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _init(rank, world, port):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+
+
+def _nbody_worker(rank, world, port, n, steps, out_path):
+    _init(rank, world, port)
+    from paper_2411_18889_b200.distributed import ShardedLeapfrog
+    from paper_2411_18889_b200.nbody import plummer_numpy
+
+    pos, vel = plummer_numpy(n, 21)
+    nl = n // world
+    sim = ShardedLeapfrog(torch.from_numpy(pos[rank * nl:(rank + 1) * nl]),
+                          torch.from_numpy(vel[rank * nl:(rank + 1) * nl]), 2.0 ** -6, 2.0 ** -7,
+                          kernels=OracleNBodyKernels(64))
+    sim.step(steps)
+    gp = [torch.empty_like(sim.pos) for _ in range(world)]
+    gv = [torch.empty_like(sim.vel) for _ in range(world)]
+    ga = [torch.empty_like(sim.acc) for _ in range(world)]
+    dist.all_gather(gp, sim.pos.clone())
+    dist.all_gather(gv, sim.vel)
+    dist.all_gather(ga, sim.acc)
+    if rank == 0:
+        np.savez(out_path, pos=torch.cat(gp).numpy(), vel=torch.cat(gv).numpy(), acc=torch.cat(ga).numpy())
+    dist.destroy_process_group()
+
+
+def _diff_worker(rank, world, port, shape, steps, out_path):
+    _init(rank, world, port)
+    from paper_2411_18889_b200.distributed import SlabDiffusion
+
+    f0 = np.random.default_rng(4).random(shape, dtype=np.float32)
+    args = (0.1, 0.12, 0.09, 1e-3, 1.0)
+    counts = [shape[0] // world + (1 if r < shape[0] % world else 0) for r in range(world)]
+    lo = sum(counts[:rank])
+    sim = SlabDiffusion(torch.from_numpy(f0[lo:lo + counts[rank]].copy()), *args, kernels=OracleSlabKernels(*args))
+    sim.step(steps)
+    parts = [None] * world
+    dist.all_gather_object(parts, sim.f.numpy())
+    if rank == 0:
+        np.save(out_path, np.concatenate(parts, axis=0))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_sharded_leapfrog_equals_unsharded(tmp_path, world):
+    n, steps = 512, 3
+    out = tmp_path / "nbody.npz"
+    mp.spawn(_nbody_worker, args=(world, _free_port(), n, steps, str(out)), nprocs=world, join=True)
+    got = np.load(out)
+    # unsharded: world 1 through the same class and kernels
+    out1 = tmp_path / "nbody1.npz"
+    mp.spawn(_nbody_worker, args=(1, _free_port(), n, steps, str(out1)), nprocs=1, join=True)
+    want = np.load(out1)
+    for k in ("pos", "vel", "acc"):
+        assert np.array_equal(got[k].view(np.uint32), want[k].view(np.uint32)), k
+
+
+def test_unsharded_chunked_leapfrog_tracks_reference_kdk(tmp_path):
+    """The chunked structure stays within FP32 tolerance of the plain oracle KDK."""
+    import oracle
+
+    from paper_2411_18889_b200.nbody import plummer_numpy
+
+    n, steps = 512, 3
+    out1 = tmp_path / "nbody1.npz"
+    mp.spawn(_nbody_worker, args=(1, _free_port(), n, steps, str(out1)), nprocs=1, join=True)
+    got = np.load(out1)
+    pos, vel = plummer_numpy(n, 21)
+    wp, wv, wa = oracle.Restatement().leapfrog(pos, vel, 2.0 ** -6, 2.0 ** -7, steps)
+    assert np.linalg.norm(got["pos"] - wp) / np.linalg.norm(wp) < 1e-6
+    assert np.linalg.norm(got["acc"] - wa) / np.linalg.norm(wa) < 1e-5
+
+
+@pytest.mark.parametrize("world,shape", [(2, (12, 9, 10)), (3, (10, 7, 8)), (2, (4, 5, 6))])
+def test_slab_diffusion_equals_full_grid(tmp_path, world, shape):
+    import oracle
+
+    steps = 4
+    out = tmp_path / "diff.npy"
+    mp.spawn(_diff_worker, args=(world, _free_port(), shape, steps, str(out)), nprocs=world, join=True)
+    got = np.load(out)
+    f0 = np.random.default_rng(4).random(shape, dtype=np.float32)
+    want = oracle.Restatement().diffusion_run(f0, steps, 0.1, 0.12, 0.09, 1e-3, 1.0)
+    assert np.array_equal(got.view(np.uint32), want.view(np.uint32))
+
+
+def test_shard_plan_requires_divisible_n():
+    from paper_2411_18889_b200.distributed import ShardPlan
+
+    p = ShardPlan(1 << 22, 8, 3)
+    assert (p.n_local, p.lo, p.hi) == (1 << 19, 3 << 19, 4 << 19)
