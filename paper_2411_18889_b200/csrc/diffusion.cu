@@ -23,6 +23,7 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 
 #include "common.cuh"
 
@@ -113,7 +114,7 @@ struct MarchArgs {
 };
 
 template <int S>
-__global__ void __launch_bounds__(kMarchThreads, 2) k_diffusion_march(const MarchArgs a) {
+__global__ void __launch_bounds__(kMarchThreads, (S <= 2 ? 4 : 2)) k_diffusion_march(const MarchArgs a) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int nz = a.nz, ny = a.ny, nx = a.nx;
   const int nz4 = nz >> 2;
@@ -266,20 +267,29 @@ struct MarchPlan {
   size_t smem = 0;
 };
 
+static int env_int(const char* name, int dflt) {  // tuning knobs for bench sweeps
+  const char* e = std::getenv(name);
+  return e ? std::atoi(e) : dflt;
+}
+
 static bool plan_march(int nx_out, int ny, int nz, MarchPlan& mp) {
   if (nz % 4 != 0 || nz < 4) return false;
   const int nz4 = nz / 4;
   const DeviceInfo& di = device_info();
-  // Choose S (cells/thread/4) so a tile has >= 2 rows and fits 3+ stages in
-  // half the SM's shared memory (two CTAs per SM).
+  static const int occ = std::max(1, env_int("SOLOMON_DIFF_OCC", 2));
+  static const int max_nst = std::max(2, env_int("SOLOMON_DIFF_NST", 3));  // 3 beat 2 and 4 (round-1 sweep)
+  static const int force_s = env_int("SOLOMON_DIFF_S", 0);
+  static const int force_splits = env_int("SOLOMON_DIFF_SPLITS", 0);
+  // Choose S (cells/thread/4) so the stages of `occ` CTAs fit one SM's shared memory.
   static const int kS[] = {4, 8, 2, 1};
   for (int S : kS) {
+    if (force_s && S != force_s) continue;
     int TJ = (kMarchThreads * S) / nz4;
     if (TJ < 1) continue;
     TJ = std::min(TJ, ny);
     const size_t stage = static_cast<size_t>(TJ + 2) * nz * sizeof(float);
-    const size_t budget = std::min<size_t>(di.smem_optin, 227 * 1024) / 2 - 128;
-    int nst = static_cast<int>(std::min<size_t>(4, budget / stage));
+    const size_t budget = (228 * 1024) / occ - 1024 - 128;
+    int nst = static_cast<int>(std::min<size_t>(max_nst, budget / stage));
     if (nst < 2) continue;
     mp.S = S;
     mp.TJ = TJ;
@@ -290,10 +300,10 @@ static bool plan_march(int nx_out, int ny, int nz, MarchPlan& mp) {
   if (!mp.S) return false;
   mp.n_jtiles = (ny + mp.TJ - 1) / mp.TJ;
   // Single co-resident wave when possible: split i so that n_jtiles * splits
-  // fills the 2-CTA-per-SM residency; neighbours then march in lock step and
-  // share halo rows/planes through L2.
-  const int resident = 2 * di.sms;
-  int splits = std::max(1, resident / mp.n_jtiles);
+  // fills the residency; neighbours then march in lock step and share halo
+  // rows/planes through L2.
+  const int resident = occ * di.sms;
+  int splits = force_splits ? force_splits : std::max(1, resident / mp.n_jtiles);
   splits = std::min(splits, std::max(1, nx_out / 4));
   mp.IC = (nx_out + splits - 1) / splits;
   mp.grid = mp.n_jtiles * ((nx_out + mp.IC - 1) / mp.IC);
@@ -312,7 +322,7 @@ static int launch_step(int nx, int ny, int nz, const Coefs& c, const float* f, c
   case SV: {                                                                                                  \
     static bool attr_set = false;                                                                             \
     if (!attr_set) {                                                                                          \
-      cudaFuncSetAttribute(k_diffusion_march<SV>, cudaFuncAttributeMaxDynamicSharedMemorySize, 113 * 1024); \
+      cudaFuncSetAttribute(k_diffusion_march<SV>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024); \
       attr_set = true;                                                                                        \
     }                                                                                                         \
     k_diffusion_march<SV><<<mp.grid, kMarchThreads, mp.smem, s>>>(a);                                         \

@@ -290,16 +290,16 @@ struct ForceVariant {
 #define B2_FV(B, I, M, U, S) \
   { B, I, { k_force_fast<B, I, M, U, S, false>, k_force_fast<B, I, M, U, S, true> } }
 static const ForceVariant kVariants[] = {
-    B2_FV(256, 8, 2, 4, 1),  // 0: default for large N
-    B2_FV(64, 8, 8, 4, 1),   // 1: small N (more CTAs)
-    B2_FV(256, 8, 2, 4, 0),  // 2: depth-first schedule (round-1 baseline)
-    B2_FV(256, 4, 4, 8, 0),  // 3
-    B2_FV(256, 4, 4, 8, 1),  // 4
-    B2_FV(256, 8, 2, 2, 1),  // 5
-    B2_FV(128, 8, 4, 4, 1),  // 6
-    B2_FV(256, 4, 3, 4, 1),  // 7
-    B2_FV(256, 12, 1, 2, 1), // 8
-    B2_FV(256, 4, 4, 4, 1),  // 9
+    B2_FV(256, 12, 1, 2, 1),  // 0: default for large N (best of the round-1 sweep)
+    B2_FV(64, 8, 8, 4, 1),    // 1: small N (more CTAs)
+    B2_FV(256, 8, 2, 4, 0),   // 2: round-1 first version
+    B2_FV(256, 4, 4, 8, 0),   // 3
+    B2_FV(128, 12, 2, 2, 1),  // 4
+    B2_FV(256, 16, 1, 2, 1),  // 5
+    B2_FV(256, 12, 1, 4, 1),  // 6
+    B2_FV(128, 16, 2, 1, 1),  // 7
+    B2_FV(256, 10, 1, 2, 1),  // 8
+    B2_FV(256, 12, 1, 1, 1),  // 9
 };
 #undef B2_FV
 
