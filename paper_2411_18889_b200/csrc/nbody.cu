@@ -40,6 +40,17 @@ __device__ __forceinline__ float rsqrt_approx(float x) {
   return r;
 }
 
+__device__ __forceinline__ float ex2_approx(float x) {
+  float r;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+__device__ __forceinline__ float lg2_approx(float x) {
+  float r;
+  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+
 // ---------------------------------------------------------------------------
 // K1 fast: packed-FP32 tile kernel.
 // grid.x = n_itiles * nchunks; block = BLOCK threads; out = partials[c][Ni].
@@ -110,12 +121,60 @@ __device__ __forceinline__ void interact_df(const float2 X, const float2 Y, cons
   }
 }
 
-template <int BLOCK, int kIPT, int MINB, int UNR, int SCHED, bool POT>
+// Pairs [0, P-ALT) on the reference formula (rsqrt, cube, mass), pairs
+// [P-ALT, P) on s = ex2(fma(-1.5, lg2(r2), lg2(m_j))).
+template <int P, int ALT, bool POT>
+__device__ __forceinline__ void interact_mixed(const float2 X, const float2 Y, const float2 Z, const float2 M,
+                                               const float LM, const float2 (&nx)[P], const float2 (&ny)[P],
+                                               const float2 (&nz)[P], const float2 e2, float2 (&ax)[P],
+                                               float2 (&ay)[P], float2 (&az)[P], float2 (&ap)[P]) {
+  const float2 lm = make_float2(LM, LM);
+  const float2 k15 = make_float2(-1.5f, -1.5f);
+#pragma unroll
+  for (int p = 0; p < P; ++p) {
+    const float2 rx = __fadd2_rn(X, nx[p]);
+    const float2 ry = __fadd2_rn(Y, ny[p]);
+    const float2 rz = __fadd2_rn(Z, nz[p]);
+    float2 r2 = __ffma2_rn(rx, rx, e2);
+    r2 = __ffma2_rn(ry, ry, r2);
+    r2 = __ffma2_rn(rz, rz, r2);
+    float2 w;
+    if (p < P - ALT) {
+      w = make_float2(rsqrt_approx(r2.x), rsqrt_approx(r2.y));
+      w = __fmul2_rn(w, __fmul2_rn(w, w));
+      w = __fmul2_rn(w, M);
+    } else {
+      const float2 l = make_float2(lg2_approx(r2.x), lg2_approx(r2.y));
+      const float2 y = __ffma2_rn(l, k15, lm);
+      w = make_float2(ex2_approx(y.x), ex2_approx(y.y));
+    }
+    ax[p] = __ffma2_rn(rx, w, ax[p]);
+    ay[p] = __ffma2_rn(ry, w, ay[p]);
+    az[p] = __ffma2_rn(rz, w, az[p]);
+    if (POT) ap[p] = __ffma2_rn(r2, w, ap[p]);
+  }
+}
+
+// SCHED: 0 depth-first / 1 breadth-first source order (ptxas mostly reschedules).
+// SCHED 2: j-values kept NON-duplicated in shared memory and fed to the packed
+// ops as scalar-broadcast operands (FADD2 R, R.F32x2, R.F32): one LDS.128 per j
+// and one fewer register-pair read per FADD2/FMUL2 -- the register file read
+// bandwidth, not the FMA datapath, is what caps this loop (probe: FFMA2 with
+// three distinct register pairs runs at 52% of peak).
+//
+// ALT > 0 moves the last ALT pairs of every thread onto a second formula that
+// trades FMA-pipe work for MUFU work: m r^-3 = ex2(fma(-1.5, lg2(r2), lg2(m)))
+// -- 2 MUFU + 1 FFMA2 per pair instead of 1 MUFU + 3 FMUL2 -- so the FP32
+// pipe (the binding one) and the MUFU pipe (58% busy) are balanced.
+template <int BLOCK, int kIPT, int MINB, int UNR, int SCHED, int ALT, bool POT>
 __global__ void __launch_bounds__(BLOCK, MINB)
     k_force_fast(const float4* __restrict__ ipos, int Ni, const float4* __restrict__ jpos, int Nj,
                  int jchunk, int n_itiles, float eps2, float4* __restrict__ out) {
   constexpr int P = kIPT / 2;
-  __shared__ float4 sj[2][2 * BLOCK];
+  constexpr int DUP = SCHED >= 2 ? 1 : 2;  // float4 slots per j in shared memory
+  static_assert(ALT == 0 || DUP == 1, "ALT path uses scalar-broadcast j");
+  __shared__ float4 sj[2][DUP * BLOCK];
+  __shared__ float slm[2][ALT > 0 ? BLOCK : 1];
 
   const int tid = threadIdx.x;
   const int itile = blockIdx.x % n_itiles;
@@ -148,8 +207,13 @@ __global__ void __launch_bounds__(BLOCK, MINB)
     return j < j1 ? __ldg(jpos + j) : make_float4(0.f, 0.f, 0.f, 0.f);
   };
   auto stash = [&](int buf, float4 pj) {
-    sj[buf][2 * tid + 0] = make_float4(pj.x, pj.x, pj.y, pj.y);
-    sj[buf][2 * tid + 1] = make_float4(pj.z, pj.z, pj.w, pj.w);
+    if (DUP == 1) {
+      sj[buf][tid] = pj;
+      if (ALT > 0) slm[buf][tid] = lg2_approx(pj.w);  // -inf for m = 0: contributes 0
+    } else {
+      sj[buf][2 * tid + 0] = make_float4(pj.x, pj.x, pj.y, pj.y);
+      sj[buf][2 * tid + 1] = make_float4(pj.z, pj.z, pj.w, pj.w);
+    }
   };
 
   stash(0, fetch(0));
@@ -164,13 +228,26 @@ __global__ void __launch_bounds__(BLOCK, MINB)
     const float4* __restrict__ s = sj[buf];
 #pragma unroll UNR
     for (int jj = 0; jj < BLOCK; ++jj) {
-      const float4 A = s[2 * jj + 0];
-      const float4 B = s[2 * jj + 1];
-      const float2 X = make_float2(A.x, A.y);
-      const float2 Y = make_float2(A.z, A.w);
-      const float2 Z = make_float2(B.x, B.y);
-      const float2 M = make_float2(B.z, B.w);
-      if (SCHED == 1)
+      float2 X, Y, Z, M;
+      float LM = 0.f;
+      if (ALT > 0) LM = slm[buf][jj];
+      if (DUP == 1) {
+        const float4 q = s[jj];
+        X = make_float2(q.x, q.x);
+        Y = make_float2(q.y, q.y);
+        Z = make_float2(q.z, q.z);
+        M = make_float2(q.w, q.w);
+      } else {
+        const float4 A = s[2 * jj + 0];
+        const float4 B = s[2 * jj + 1];
+        X = make_float2(A.x, A.y);
+        Y = make_float2(A.z, A.w);
+        Z = make_float2(B.x, B.y);
+        M = make_float2(B.z, B.w);
+      }
+      if (ALT > 0)
+        interact_mixed<P, ALT, POT>(X, Y, Z, M, LM, nx, ny, nz, e2, ax, ay, az, ap);
+      else if (SCHED >= 1)
         interact_bf<P, POT>(X, Y, Z, M, nx, ny, nz, e2, ax, ay, az, ap);
       else
         interact_df<P, POT>(X, Y, Z, M, nx, ny, nz, e2, ax, ay, az, ap);
@@ -287,19 +364,19 @@ struct ForceVariant {
   int block, ipt;
   void (*fn[2])(const float4*, int, const float4*, int, int, int, float, float4*);
 };
-#define B2_FV(B, I, M, U, S) \
-  { B, I, { k_force_fast<B, I, M, U, S, false>, k_force_fast<B, I, M, U, S, true> } }
+#define B2_FV(B, I, M, U, S, A) \
+  { B, I, { k_force_fast<B, I, M, U, S, A, false>, k_force_fast<B, I, M, U, S, A, true> } }
 static const ForceVariant kVariants[] = {
-    B2_FV(256, 12, 1, 2, 1),  // 0: default for large N (best of the round-1 sweep)
-    B2_FV(64, 8, 8, 4, 1),    // 1: small N (more CTAs)
-    B2_FV(256, 8, 2, 4, 0),   // 2: round-1 first version
-    B2_FV(256, 4, 4, 8, 0),   // 3
-    B2_FV(128, 12, 2, 2, 1),  // 4
-    B2_FV(256, 16, 1, 2, 1),  // 5
-    B2_FV(256, 12, 1, 4, 1),  // 6
-    B2_FV(128, 16, 2, 1, 1),  // 7
-    B2_FV(256, 10, 1, 2, 1),  // 8
-    B2_FV(256, 12, 1, 1, 1),  // 9
+    B2_FV(128, 16, 2, 1, 2, 0),  // 0: default for large N (best of the round-1 sweep)
+    B2_FV(64, 8, 8, 4, 1, 0),    // 1: small N (more CTAs)
+    B2_FV(256, 8, 2, 4, 0, 0),   // 2: round-1 first version
+    B2_FV(256, 12, 1, 2, 1, 0),  // 3: duplicated-pair j
+    B2_FV(128, 16, 2, 1, 3, 2),  // 4: 2 of 8 pairs on ex2/lg2
+    B2_FV(128, 16, 2, 1, 3, 3),  // 5: 3 of 8
+    B2_FV(256, 12, 1, 2, 3, 2),  // 6: 2 of 6
+    B2_FV(256, 12, 1, 2, 3, 1),  // 7: 1 of 6
+    B2_FV(128, 16, 2, 2, 3, 2),  // 8
+    B2_FV(256, 8, 2, 4, 3, 1),   // 9: 1 of 4
 };
 #undef B2_FV
 

@@ -129,3 +129,110 @@ extern "C" double solomon_probe_pattern_tflops(int mode) {
   const double lanes = (mode == 2) ? 1.0 : 2.0;
   return double(threads) * blocks * iters * 8 * 8 * lanes * 2 / (best * 1e-3) / 1e12;
 }
+
+// n-body inner-loop probes: j-particles from __constant__ (uniform datapath)
+// vs shared memory, same 12 i-particles per thread (6 packed pairs).
+__constant__ float4 c_j[4096];
+
+__device__ __forceinline__ float rsq_(float x) {
+  float r;
+  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+
+template <int SRC>  // 0: constant, 1: shared (duplicated pairs)
+__global__ void __launch_bounds__(256, 1) k_nbody_probe(const float4* __restrict__ gj, int reps, float eps2,
+                                                        float4* out) {
+  constexpr int P = 6;
+  __shared__ float4 sj[2 * 1024];
+  float2 nx[P], ny[P], nz[P], ax[P], ay[P], az[P];
+  for (int p = 0; p < P; ++p) {
+    const float f = 0.001f * (threadIdx.x + 256 * p + blockIdx.x);
+    nx[p] = make_float2(-f, -f - 0.1f);
+    ny[p] = make_float2(f * 0.5f, f * 0.3f);
+    nz[p] = make_float2(-f * 0.7f, f * 0.2f);
+    ax[p] = ay[p] = az[p] = make_float2(0.f, 0.f);
+  }
+  if (SRC == 1) {
+    for (int j = threadIdx.x; j < 1024; j += 256) {
+      const float4 q = gj[j];
+      sj[2 * j] = make_float4(q.x, q.x, q.y, q.y);
+      sj[2 * j + 1] = make_float4(q.z, q.z, q.w, q.w);
+    }
+    __syncthreads();
+  }
+  const float2 e2 = make_float2(eps2, eps2);
+  for (int r = 0; r < reps; ++r) {
+#pragma unroll 2
+    for (int j = 0; j < 1024; ++j) {
+      float2 X, Y, Z, M;
+      if (SRC == 0) {
+        const float4 q = c_j[j];
+        X = make_float2(q.x, q.x);
+        Y = make_float2(q.y, q.y);
+        Z = make_float2(q.z, q.z);
+        M = make_float2(q.w, q.w);
+      } else {
+        const float4 A = sj[2 * j], B = sj[2 * j + 1];
+        X = make_float2(A.x, A.y);
+        Y = make_float2(A.z, A.w);
+        Z = make_float2(B.x, B.y);
+        M = make_float2(B.z, B.w);
+      }
+#pragma unroll
+      for (int p = 0; p < P; ++p) {
+        const float2 rx = __fadd2_rn(X, nx[p]);
+        const float2 ry = __fadd2_rn(Y, ny[p]);
+        const float2 rz = __fadd2_rn(Z, nz[p]);
+        float2 r2 = __ffma2_rn(rx, rx, e2);
+        r2 = __ffma2_rn(ry, ry, r2);
+        r2 = __ffma2_rn(rz, rz, r2);
+        float2 w = make_float2(rsq_(r2.x), rsq_(r2.y));
+        w = __fmul2_rn(w, __fmul2_rn(w, w));
+        w = __fmul2_rn(w, M);
+        ax[p] = __ffma2_rn(rx, w, ax[p]);
+        ay[p] = __ffma2_rn(ry, w, ay[p]);
+        az[p] = __ffma2_rn(rz, w, az[p]);
+      }
+    }
+  }
+  float s = 0.f;
+  for (int p = 0; p < P; ++p) s += ax[p].x + ax[p].y + ay[p].x + ay[p].y + az[p].x + az[p].y;
+  out[blockIdx.x * 256 + threadIdx.x] = make_float4(s, 0, 0, 0);
+}
+
+// Returns achieved "20-flop" TFLOP/s of the inner loop.
+extern "C" double solomon_probe_nbody_inner(int src) {
+  float4 h[4096];
+  for (int j = 0; j < 4096; ++j) h[j] = make_float4(0.01f * (j % 97), 0.02f * (j % 89), -0.013f * (j % 83), 1e-3f);
+  cudaMemcpyToSymbol(c_j, h, sizeof(h));
+  float4 *gj = nullptr, *out = nullptr;
+  cudaMalloc(&gj, sizeof(h));
+  cudaMemcpy(gj, h, sizeof(h), cudaMemcpyHostToDevice);
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int blocks = sms * 2, reps = 64;
+  cudaMalloc(&out, sizeof(float4) * 256 * blocks);
+  auto launch = [&] {
+    if (src == 0)
+      k_nbody_probe<0><<<blocks, 256>>>(gj, reps, 1e-4f, out);
+    else
+      k_nbody_probe<1><<<blocks, 256>>>(gj, reps, 1e-4f, out);
+  };
+  launch();
+  cudaDeviceSynchronize();
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  cudaEventRecord(e0);
+  launch();
+  cudaEventRecord(e1);
+  cudaEventSynchronize(e1);
+  float ms;
+  cudaEventElapsedTime(&ms, e0, e1);
+  cudaFree(gj);
+  cudaFree(out);
+  const double inter = double(blocks) * 256 * 12 * 1024.0 * reps;
+  return 20.0 * inter / (ms * 1e-3) / 1e12;
+}
