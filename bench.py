@@ -51,6 +51,7 @@ def parse_args():
     ap.add_argument("--dsteps", type=int, default=50, help="timed diffusion steps")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-diffusion", action="store_true")
+    ap.add_argument("--no-configs", action="store_true", help="skip the BASELINE parity configs [0] and [1]")
     ap.add_argument("--cpu-seconds", type=float, default=8.0, help="target CPU time per baseline sample")
     return ap.parse_args()
 
@@ -399,6 +400,12 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         result["secondary"] = {"diffusion": run_diffusion(args, rank, world, dev, stream, peaks, barrier,
                                                           max_over_ranks, flush)}
 
+    if world == 1 and not args.no_configs:
+        try:
+            result["parity_configs"] = run_parity_configs(dev)
+        except FileNotFoundError as e:
+            result["parity_configs"] = {"unavailable": str(e)}
+
     # ---------------- CPU baseline (rank 0, N=1) ----------------
     if world == 1 and rank == 0 and not args.no_cpu_baseline:
         _omp_env()
@@ -499,6 +506,79 @@ def run_diffusion(args, rank, world, dev, stream, peaks, barrier, max_over_ranks
             except FileNotFoundError as e:
                 out["cpu_baseline"] = {"value": None, "unavailable": str(e)}
         del host_f, host_fn
+    return out
+
+
+def run_parity_configs(dev):
+    """BASELINE configs[0] and [1] (the CPU-reference-run parity cases): GPU time, CPU time, parity."""
+    import numpy as np
+    import torch
+
+    import oracle
+    import paper_2411_18889_b200 as b2
+
+    _omp_env()
+    out = {}
+    # configs[0]: N=4096 Plummer FP32, 16 leapfrog steps
+    n, eps, dt, steps = 4096, EPS, DT, 16
+    pos, vel = b2.plummer_numpy(n, 42)
+    lf = b2.Leapfrog(torch.from_numpy(pos).to(dev), torch.from_numpy(vel).to(dev), eps, dt)
+    lf.step(2)
+    lf = b2.Leapfrog(torch.from_numpy(pos).to(dev), torch.from_numpy(vel).to(dev), eps, dt)
+    torch.cuda.synchronize(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    lf.step(steps)
+    e1.record()
+    torch.cuda.synchronize(dev)
+    gpu_ms = e0.elapsed_time(e1)
+    rs = oracle.Restatement()
+    t0 = time.perf_counter()
+    wp, wv, wa = rs.leapfrog(pos, vel, eps, dt, steps)
+    cpu_ms = (time.perf_counter() - t0) * 1e3
+    gp, gv = lf.pos.cpu().numpy(), lf.vel.cpu().numpy()
+    rel = lambda a, b: float(np.linalg.norm(a - b) / np.linalg.norm(b))  # noqa: E731
+    out["nbody_4096_plummer_kdk16"] = {
+        "config": "BASELINE configs[0]: N=4096 Plummer FP32, 16 leapfrog steps",
+        "gpu_ms": gpu_ms, "gpu_launches": 2 * steps + 1,
+        "gpu_ginteractions_per_s": n * n * steps / (gpu_ms * 1e-3) / 1e9,
+        "cpu_ms": cpu_ms, "cpu_kind": "port (oracle/solomon_oracle.c KDK around the restated calc_acc; "
+                                      "the reference has no integrator)",
+        "cpu_cores": int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1)),
+        "parity_relL2": {"pos": rel(gp[:, :3], wp[:, :3]), "vel": rel(gv[:, :3], wv[:, :3])},
+        "tolerance": {"pos": 1e-5, "vel": 1e-4},
+    }
+    # configs[1]: 128^3 diffusion, 100 steps
+    g, dsteps = 128, 100
+    dx = 1.0 / g
+    dargs = (dx, dx, dx, 0.1 * dx * dx, 1.0)
+    f0 = b2.init_grid(g, g, g, seed=7, device=dev)
+    sim = b2.Diffusion3D(f0.clone(), *dargs)
+    sim.run(10)
+    sim = b2.Diffusion3D(f0.clone(), *dargs)
+    torch.cuda.synchronize(dev)
+    e0.record()
+    sim.run(dsteps)
+    e1.record()
+    torch.cuda.synchronize(dev)
+    gpu_ms = e0.elapsed_time(e1)
+    host = f0.cpu().numpy()
+    ref = oracle.Reference("ieee")
+    fast = oracle.Reference("fast")
+    t0 = time.perf_counter()
+    fast.diffusion_run(host, dsteps, *dargs)
+    cpu_ms = (time.perf_counter() - t0) * 1e3
+    want = ref.diffusion_run(host, dsteps, *dargs)
+    got = sim.field.cpu().numpy()
+    out["diffusion_128_100steps"] = {
+        "config": "BASELINE configs[1]: 128^3 grid, 100 steps, single B200 (L2-resident: 2 x 8 MiB)",
+        "gpu_ms": gpu_ms, "gpu_launches": dsteps, "gpu_glups": g ** 3 * dsteps / (gpu_ms * 1e-3) / 1e9,
+        "cpu_ms": cpu_ms, "cpu_kind": "reference (oracle/_ref libref_fast)",
+        "cpu_glups": g ** 3 * dsteps / (cpu_ms * 1e-3) / 1e9,
+        "cpu_cores": int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1)),
+        "parity": "bit-identical" if np.array_equal(got.view(np.uint32), want.view(np.uint32)) else
+                  f"MISMATCH relL2 {rel(got, want):.3e}",
+    }
     return out
 
 

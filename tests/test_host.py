@@ -79,3 +79,17 @@ def test_package_does_not_import_oracle():
         assert not re.search(r"^\s*(import|from)\s+oracle", py.read_text(), flags=re.M), py
     for cu in (pkg / "csrc").glob("*.c*"):
         assert "oracle" not in cu.read_text().lower() or cu.name == "probe.cu", cu
+
+
+def test_residency_requires_mapping():
+    from paper_2411_18889_b200 import residency as R
+
+    a = np.zeros(8, np.float32)
+    assert not R.is_present(a)
+    with pytest.raises(b2.SolomonError):
+        R.present(a)
+    with pytest.raises(b2.SolomonError):
+        R.free_from_device(a)
+    if not torch.cuda.is_available():
+        with pytest.raises(b2.SolomonError):
+            R.malloc_on_device(a)

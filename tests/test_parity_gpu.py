@@ -265,3 +265,25 @@ def test_dropin_reports_invalid_arguments(b2):
 def test_python_api_rejects_cpu_tensors(b2):
     with pytest.raises(b2.SolomonError):
         b2.accelerations(torch.zeros(4, 4), 0.1)
+
+
+def test_residency_helpers_present_contract(b2, golden):
+    """MALLOC_ON_DEVICE / MEMCPY_H2D / present / MEMCPY_D2H around the diffusion3d drop-in."""
+    from paper_2411_18889_b200 import residency as R
+
+    f0 = np.ascontiguousarray(golden["diff/cube16/f0"]).copy()
+    dx, dy, dz, dt, kappa = (float(v) for v in golden["diff/cube16/params"])
+    steps = int(golden["diff/cube16/steps"])
+    fn = np.empty_like(f0)
+    with R.data_access_by_device(copy=[f0], create=[fn]):
+        a, b = R.present(f0), R.present(fn)
+        for _ in range(steps):
+            b2.diffusion3d(*f0.shape, dx, dy, dz, dt, kappa, a, b)
+            a, b = b, a
+        if steps % 2:
+            a_host = a  # result lives in fn's mirror; copy it into f0's for copy-out
+            R.present(f0).copy_(a_host)
+    assert bits_equal(f0, golden["diff/cube16/f"])
+    assert not R.is_present(f0) and not R.is_present(fn)
+    with pytest.raises(b2.SolomonError):
+        R.present(f0)
