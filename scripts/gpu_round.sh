@@ -1,10 +1,12 @@
+# Round evidence: GPU tests, smoke, bench (both arms), ncu launch list, ncu --set full of the two hot kernels.
 set -x
+TAG=${TAG:-r01}
 mkdir -p gpurun_out
 python -m pytest tests -m gpu -x -q 2>&1 | tail -5
 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -3
-python bench.py > gpurun_out/bench_r01.json 2> gpurun_out/bench_r01.err; tail -3 gpurun_out/bench_r01.err
-python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/bench_ref_r01.json 2>&1
-ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_r01.csv python bench.py --steps 2 --warmup 1 --no-cpu-baseline --dsteps 10 > /dev/null 2>&1
-ncu --set full --clock-control none --import-source on -k regex:k_force_fast -s 2 -c 1 -o gpurun_out/prof_force_r01 python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-diffusion > gpurun_out/ncu_force.log 2>&1
-ncu --set full --clock-control none --import-source on -k regex:k_diffusion_march -s 5 -c 1 -o gpurun_out/prof_diff_r01 python bench.py --steps 1 --warmup 0 --no-cpu-baseline --dsteps 2 --n 65536 > gpurun_out/ncu_diff.log 2>&1
+python bench.py > gpurun_out/bench_$TAG.json 2> gpurun_out/bench_$TAG.err; tail -3 gpurun_out/bench_$TAG.err
+python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/bench_ref_$TAG.json 2>&1
+ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_$TAG.csv python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-configs --dsteps 10 > /dev/null 2>&1
+ncu --set full --clock-control none --import-source on -k regex:k_force_fast -s 2 -c 1 -o gpurun_out/prof_force_$TAG python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-diffusion --no-configs > /dev/null 2>&1
+ncu --set full --clock-control none --import-source on -k regex:k_diffusion_march -s 5 -c 1 -o gpurun_out/prof_diff_$TAG python bench.py --steps 1 --warmup 0 --no-cpu-baseline --no-configs --dsteps 2 --n 65536 > /dev/null 2>&1
 ls -la gpurun_out
