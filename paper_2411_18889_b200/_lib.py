@@ -89,5 +89,35 @@ def require_cuda(t: torch.Tensor, name: str) -> None:
         raise SolomonError(f"{name} must be a CUDA tensor (no CPU fallback); got device {t.device}")
 
 
+_raw_stream = getattr(torch._C, "_cuda_getCurrentRawStream", None)
+
+
 def stream_handle(device: torch.device | None = None) -> int:
+    """cudaStream_t of torch's current stream on ``device`` (cheap path when available)."""
+    if _raw_stream is not None:
+        idx = device.index if isinstance(device, torch.device) and device.index is not None else \
+            torch.cuda.current_device()
+        return _raw_stream(idx)
     return torch.cuda.current_stream(device).cuda_stream
+
+
+class on_device:
+    """``torch.cuda.device(t.device)`` only when it differs from the current device."""
+
+    __slots__ = ("idx", "prev")
+
+    def __init__(self, device: torch.device):
+        self.idx = device.index if device.index is not None else torch.cuda.current_device()
+        self.prev = None
+
+    def __enter__(self):
+        cur = torch.cuda.current_device()
+        if cur != self.idx:
+            self.prev = cur
+            torch.cuda.set_device(self.idx)
+        return self
+
+    def __exit__(self, *exc):
+        if self.prev is not None:
+            torch.cuda.set_device(self.prev)
+        return False

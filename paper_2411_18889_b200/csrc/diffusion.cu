@@ -19,6 +19,7 @@
 // -O3 contracts it: v = ce*f_ip; v = fma(cc, f, v); then
 // fma(cw,f_im), fma(cn,f_jp), fma(cs,f_jm), fma(ct,f_kp), fma(cb,f_km) --
 // bit-identical to the reference build.
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -261,6 +262,88 @@ __global__ void __launch_bounds__(256)
 }
 
 // ---------------------------------------------------------------------------
+// Direct kernel for L2-resident grids (configs[1]: 128^3 = 2 x 8 MiB): one
+// thread per 4 consecutive k cells, every neighbour straight from L1/L2 with
+// 16-byte loads. No staging pipeline to fill, so short steps are not
+// latency-bound on the march kernel's prologue. Requires nz % 4 == 0 and
+// 16-byte aligned f / fn; same arithmetic (bit-identical).
+__global__ void __launch_bounds__(256)
+    k_diffusion_direct(const float* __restrict__ f, const float* __restrict__ halo_lo,
+                       const float* __restrict__ halo_hi, float* __restrict__ fn, int nx, int ny, int nz,
+                       int i_begin, int i_end, Coefs c) {
+  const int nz4 = nz >> 2;
+  const size_t plane = static_cast<size_t>(ny) * nz;
+  const size_t total = static_cast<size_t>(i_end - i_begin) * ny * nz4;
+  for (size_t t = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; t < total;
+       t += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    const int c4 = static_cast<int>(t % nz4);
+    const size_t r = t / nz4;
+    const int j = static_cast<int>(r % ny);
+    const int i = i_begin + static_cast<int>(r / ny);
+    const float* P = f + static_cast<size_t>(i) * plane;
+    const float* Pm = i > 0 ? P - plane : (halo_lo ? halo_lo : P);
+    const float* Pp = i < nx - 1 ? P + plane : (halo_hi ? halo_hi : P);
+    const size_t jk = static_cast<size_t>(j) * nz + 4 * c4;
+    const float4 fc = __ldg(reinterpret_cast<const float4*>(P + jk));
+    const float4 fip = __ldg(reinterpret_cast<const float4*>(Pp + jk));
+    const float4 fim = __ldg(reinterpret_cast<const float4*>(Pm + jk));
+    const float4 fjp = __ldg(reinterpret_cast<const float4*>(P + static_cast<size_t>(min(j + 1, ny - 1)) * nz + 4 * c4));
+    const float4 fjm = __ldg(reinterpret_cast<const float4*>(P + static_cast<size_t>(max(j - 1, 0)) * nz + 4 * c4));
+    const float kl = c4 > 0 ? __ldg(P + jk - 1) : fc.x;
+    const float kr = c4 + 1 < nz4 ? __ldg(P + jk + 4) : fc.w;
+    float4 o;
+    o.x = cell(c, fc.x, fip.x, fim.x, fjp.x, fjm.x, fc.y, kl);
+    o.y = cell(c, fc.y, fip.y, fim.y, fjp.y, fjm.y, fc.z, fc.x);
+    o.z = cell(c, fc.z, fip.z, fim.z, fjp.z, fjm.z, fc.w, fc.y);
+    o.w = cell(c, fc.w, fip.w, fim.w, fjp.w, fjm.w, kr, fc.z);
+    *reinterpret_cast<float4*>(fn + static_cast<size_t>(i) * plane + jk) = o;
+  }
+}
+
+// Multi-step persistent variant for L2-resident grids (SURVEY.md §8f row 1:
+// device-resident time loop): one cooperative launch runs nsteps steps with a
+// grid-wide barrier between them, so a 128^3 step costs its L2 traffic, not a
+// kernel launch. Ping-pongs a <-> b; same arithmetic as k_diffusion_direct.
+__global__ void __launch_bounds__(256)
+    k_diffusion_multi(float* a, float* b, int nx, int ny, int nz, int nsteps, Coefs c) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  const int nz4 = nz >> 2;
+  const size_t plane = static_cast<size_t>(ny) * nz;
+  const size_t total = static_cast<size_t>(nx) * ny * nz4;
+  for (int st = 0; st < nsteps; ++st) {
+    const float* f = (st & 1) ? b : a;
+    float* fn = (st & 1) ? a : b;
+    for (size_t t = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; t < total;
+         t += static_cast<size_t>(gridDim.x) * blockDim.x) {
+      const int c4 = static_cast<int>(t % nz4);
+      const size_t r = t / nz4;
+      const int j = static_cast<int>(r % ny);
+      const int i = static_cast<int>(r / ny);
+      const float* P = f + static_cast<size_t>(i) * plane;
+      const float* Pm = i > 0 ? P - plane : P;
+      const float* Pp = i < nx - 1 ? P + plane : P;
+      const size_t jk = static_cast<size_t>(j) * nz + 4 * c4;
+      // plain (coherent) loads: f was written by other CTAs earlier in this launch
+      const float4 fc = *reinterpret_cast<const float4*>(P + jk);
+      const float4 fip = *reinterpret_cast<const float4*>(Pp + jk);
+      const float4 fim = *reinterpret_cast<const float4*>(Pm + jk);
+      const float4 fjp = *reinterpret_cast<const float4*>(P + static_cast<size_t>(min(j + 1, ny - 1)) * nz + 4 * c4);
+      const float4 fjm = *reinterpret_cast<const float4*>(P + static_cast<size_t>(max(j - 1, 0)) * nz + 4 * c4);
+      const float kl = c4 > 0 ? P[jk - 1] : fc.x;
+      const float kr = c4 + 1 < nz4 ? P[jk + 4] : fc.w;
+      float4 o;
+      o.x = cell(c, fc.x, fip.x, fim.x, fjp.x, fjm.x, fc.y, kl);
+      o.y = cell(c, fc.y, fip.y, fim.y, fjp.y, fjm.y, fc.z, fc.x);
+      o.z = cell(c, fc.z, fip.z, fim.z, fjp.z, fjm.z, fc.w, fc.y);
+      o.w = cell(c, fc.w, fip.w, fim.w, fjp.w, fjm.w, kr, fc.z);
+      *reinterpret_cast<float4*>(fn + static_cast<size_t>(i) * plane + jk) = o;
+    }
+    grid.sync();
+  }
+}
+
+// ---------------------------------------------------------------------------
 // Host planning.
 struct MarchPlan {
   int S = 0, TJ = 0, nst = 0, n_jtiles = 0, IC = 0, grid = 0;
@@ -315,6 +398,15 @@ static int launch_step(int nx, int ny, int nz, const Coefs& c, const float* f, c
   if (i_end <= i_begin) return B2_OK;
   MarchPlan mp;
   const bool ok_align = aligned16(f) && aligned16(fn) && (!lo || aligned16(lo)) && (!hi || aligned16(hi));
+  // Grids whose two fields sit comfortably in L2 take the direct kernel.
+  static const long long direct_max = env_int("SOLOMON_DIFF_DIRECT_MAXCELLS", 1 << 22);
+  const long long cells = static_cast<long long>(i_end - i_begin) * ny * nz;
+  if (ok_align && nz % 4 == 0 && cells <= direct_max) {
+    const long long work = cells / 4;
+    const int grid = static_cast<int>(std::min<long long>((work + 255) / 256, 148LL * 16));
+    k_diffusion_direct<<<grid, 256, 0, s>>>(f, lo, hi, fn, nx, ny, nz, i_begin, i_end, c);
+    return launch_status();
+  }
   if (ok_align && plan_march(i_end - i_begin, ny, nz, mp)) {
     MarchArgs a{f, lo, hi, fn, nx, ny, nz, mp.TJ, mp.n_jtiles, i_begin, i_end, mp.IC, mp.nst, c};
     switch (mp.S) {
@@ -378,6 +470,24 @@ int b2_diffusion3d_run(int nx, int ny, int nz, float dx, float dy, float dz, flo
   if (nsteps < 0) return B2_EINVAL;
   const Coefs c = make_coefs(dx, dy, dz, dt, kappa);
   cudaStream_t s = as_stream(stream);
+  static const long long direct_max = env_int("SOLOMON_DIFF_DIRECT_MAXCELLS", 1 << 22);
+  static const int use_multi = env_int("SOLOMON_DIFF_MULTI", 1);
+  const long long cells = static_cast<long long>(nx) * ny * nz;
+  if (use_multi && nsteps > 1 && nz % 4 == 0 && aligned16(f) && aligned16(fn) && cells <= direct_max) {
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_diffusion_multi, 256, 0);
+    const long long work = (cells / 4 + 255) / 256;
+    const int grid = static_cast<int>(std::min<long long>(work, static_cast<long long>(per_sm) * device_info().sms));
+    if (grid > 0) {
+      int nxv = nx, nyv = ny, nzv = nz, ns = nsteps;
+      Coefs cv = c;
+      void* args[] = {&f, &fn, &nxv, &nyv, &nzv, &ns, &cv};
+      cudaError_t e = cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(k_diffusion_multi), grid, 256, args,
+                                                  0, s);
+      if (e == cudaSuccess) return B2_OK;
+      cudaGetLastError();  // fall through to per-step launches
+    }
+  }
   float* a = f;
   float* b = fn;
   for (int st = 0; st < nsteps; ++st) {

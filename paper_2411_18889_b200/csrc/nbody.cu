@@ -31,7 +31,7 @@
 
 namespace b2 {
 
-constexpr int kChunkAlign = 256;   // j-chunk sizes are multiples of this
+constexpr int kChunkAlign = 64;    // j-chunk sizes are multiples of this
 constexpr int kTargetChunks = 64;  // j-chunks per force evaluation (fast path)
 
 __device__ __forceinline__ float rsqrt_approx(float x) {
@@ -303,7 +303,7 @@ __global__ void __launch_bounds__(128)
 
 // ---------------------------------------------------------------------------
 // K2: fused reduce + kick(s) + drift. One particle per thread, float4 I/O.
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(128)
     k_kdk_update(int n, float4* __restrict__ pos, float4* __restrict__ vel, float4* __restrict__ acc,
                  const float4* __restrict__ partials, int nchunks, float h_end, float h_begin, float dt,
                  int phases) {
@@ -311,13 +311,24 @@ __global__ void __launch_bounds__(256)
   if (i >= n) return;
   float4 a;
   if (phases & B2_KDK_REDUCE) {
+    // Fixed summation order c = 0, 1, ..., nchunks-1; loads are issued a batch
+    // at a time so the chain is bound by the adds, not by 64 serial round trips.
+    constexpr int B = 16;
     a = __ldcs(partials + i);
-    for (int c = 1; c < nchunks; ++c) {
-      const float4 p = __ldcs(partials + static_cast<size_t>(c) * n + i);
-      a.x = __fadd_rn(a.x, p.x);
-      a.y = __fadd_rn(a.y, p.y);
-      a.z = __fadd_rn(a.z, p.z);
-      a.w = __fadd_rn(a.w, p.w);
+    for (int c0 = 1; c0 < nchunks; c0 += B) {
+      float4 p[B];
+#pragma unroll
+      for (int b = 0; b < B; ++b)
+        if (c0 + b < nchunks) p[b] = __ldcs(partials + static_cast<size_t>(c0 + b) * n + i);
+#pragma unroll
+      for (int b = 0; b < B; ++b) {
+        if (c0 + b < nchunks) {
+          a.x = __fadd_rn(a.x, p[b].x);
+          a.y = __fadd_rn(a.y, p[b].y);
+          a.z = __fadd_rn(a.z, p[b].z);
+          a.w = __fadd_rn(a.w, p[b].w);
+        }
+      }
     }
     acc[i] = a;
   } else {
@@ -368,7 +379,7 @@ struct ForceVariant {
   { B, I, { k_force_fast<B, I, M, U, S, A, false>, k_force_fast<B, I, M, U, S, A, true> } }
 static const ForceVariant kVariants[] = {
     B2_FV(128, 16, 2, 1, 2, 0),  // 0: default for large N (best of the round-1 sweep)
-    B2_FV(64, 8, 8, 4, 1, 0),    // 1: small N (more CTAs)
+    B2_FV(64, 8, 8, 4, 1, 0),    // 1: medium N (more CTAs)
     B2_FV(256, 8, 2, 4, 0, 0),   // 2: round-1 first version
     B2_FV(256, 12, 1, 2, 1, 0),  // 3: duplicated-pair j
     B2_FV(128, 16, 2, 1, 3, 2),  // 4: 2 of 8 pairs on ex2/lg2
@@ -377,6 +388,7 @@ static const ForceVariant kVariants[] = {
     B2_FV(256, 12, 1, 2, 3, 1),  // 7: 1 of 6
     B2_FV(128, 16, 2, 2, 3, 2),  // 8
     B2_FV(256, 8, 2, 4, 3, 1),   // 9: 1 of 4
+    B2_FV(64, 2, 16, 4, 2, 0),   // 10: small N (configs[0]: N=4096)
 };
 #undef B2_FV
 
@@ -403,11 +415,14 @@ static int launch_partials(int Ni, const float4* ipos, int Nj, const float4* jpo
   }
   const int jchunk = chunk_size(Nj, flags);
   const int nch = nchunks_for(Nj, flags);
-  // Small i-sets use 64-thread CTAs so that the (i-tile, j-chunk) grid still
-  // covers the 148 SMs; large ones use the tuned variant.
+  // Largest tile whose (i-tile, j-chunk) grid still fills the 148 SMs: the
+  // tuned large variant, else 64x8, else 64x2 (small N is latency-bound and
+  // needs every warp it can get).
   const ForceVariant* v = &kVariants[large_variant()];
-  const long long tiles = (Ni + v->block * v->ipt - 1) / (v->block * v->ipt);
-  if (tiles * nch < 8LL * device_info().sms) v = &kVariants[1];
+  const long long want = 4LL * device_info().sms;
+  auto ctas = [&](const ForceVariant* c) { return (long long)((Ni + c->block * c->ipt - 1) / (c->block * c->ipt)) * nch; };
+  if (ctas(v) < want) v = &kVariants[1];
+  if (ctas(v) < want) v = &kVariants[10];
   const int nit = (Ni + v->block * v->ipt - 1) / (v->block * v->ipt);
   v->fn[pot ? 1 : 0]<<<nit * nch, v->block, 0, s>>>(ipos, Ni, jpos, Nj, jchunk, nit, eps2, out);
   return launch_status();
@@ -416,7 +431,7 @@ static int launch_partials(int Ni, const float4* ipos, int Nj, const float4* jpo
 static int launch_update(int n, float4* pos, float4* vel, float4* acc, const float4* partials, int nchunks,
                          float h_end, float h_begin, float dt, int phases, cudaStream_t s) {
   if (n <= 0) return B2_OK;
-  k_kdk_update<<<(n + 255) / 256, 256, 0, s>>>(n, pos, vel, acc, partials, nchunks, h_end, h_begin, dt, phases);
+  k_kdk_update<<<(n + 127) / 128, 128, 0, s>>>(n, pos, vel, acc, partials, nchunks, h_end, h_begin, dt, phases);
   return launch_status();
 }
 

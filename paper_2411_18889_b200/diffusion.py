@@ -15,7 +15,7 @@ from dataclasses import dataclass, field
 
 import torch
 
-from ._lib import check, load, require_cuda, stream_handle
+from ._lib import check, load, on_device, require_cuda, stream_handle
 
 
 def _grid(t: torch.Tensor, n: int, name: str) -> None:
@@ -51,7 +51,7 @@ def diffusion3d(nx: int, ny: int, nz: int, dx: float, dy: float, dz: float, dt: 
     _grid(fn, n, "fn")
     if f.data_ptr() == fn.data_ptr():
         raise ValueError("f and fn must not alias (restrict, listing_diffusion.c:5)")
-    with torch.cuda.device(f.device):
+    with on_device(f.device):
         check(load().b2_diffusion3d(nx, ny, nz, dx, dy, dz, dt, kappa, f.data_ptr(), fn.data_ptr(),
                                     stream_handle(f.device)), "diffusion3d")
 
@@ -69,7 +69,7 @@ def diffusion3d_slab(f: torch.Tensor, fn: torch.Tensor, halo_lo: torch.Tensor | 
             _grid(h, ny * nz, name)
     ptr = lambda t: t.data_ptr() if t is not None else None  # noqa: E731
     i_end = nx if i_end is None else i_end
-    with torch.cuda.device(f.device):
+    with on_device(f.device):
         check(load().b2_diffusion3d_slab(nx, ny, nz, dx, dy, dz, dt, kappa, f.data_ptr(), ptr(halo_lo),
                                          ptr(halo_hi), fn.data_ptr(), i_begin, i_end, stream_handle(f.device)),
               "diffusion3d_slab")
@@ -103,7 +103,7 @@ class Diffusion3D:
 
     def run(self, nsteps: int) -> torch.Tensor:
         nx, ny, nz = self.f.shape
-        with torch.cuda.device(self.f.device):
+        with on_device(self.f.device):
             check(load().b2_diffusion3d_run(nx, ny, nz, self.dx, self.dy, self.dz, self.dt, self.kappa,
                                             self.f.data_ptr(), self._fn.data_ptr(), int(nsteps),
                                             stream_handle(self.f.device)), "diffusion3d_run")

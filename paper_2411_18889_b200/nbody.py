@@ -22,7 +22,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from ._lib import B2_EXACT, B2_POTENTIAL, check, load, require_cuda, stream_handle
+from ._lib import B2_EXACT, B2_POTENTIAL, check, load, on_device, require_cuda, stream_handle
 
 
 def _flags(potential: bool, exact: bool) -> int:
@@ -66,7 +66,7 @@ def calc_acc(Ni: int, ipos: torch.Tensor, iacc: torch.Tensor, Nj: int, jpos: tor
         ws = torch.empty(need, dtype=torch.uint8, device=ipos.device)
     wptr = ws.data_ptr() if ws is not None else None
     wlen = ws.numel() if ws is not None else 0
-    with torch.cuda.device(ipos.device):
+    with on_device(ipos.device):
         check(lib.b2_calc_acc(Ni, ipos.data_ptr(), iacc.data_ptr(), Nj, jpos.data_ptr(), float(eps), flags,
                               wptr, wlen, stream_handle(ipos.device)), "calc_acc")
 
@@ -85,7 +85,7 @@ def kdk_update(pos: torch.Tensor | None, vel: torch.Tensor | None, acc: torch.Te
     """Fused K2 update (b2_kdk_update): reduce j-chunk partials, closing kick, opening kick + drift."""
     n = acc.shape[0]
     ptr = lambda t: t.data_ptr() if t is not None else None  # noqa: E731
-    with torch.cuda.device(acc.device):
+    with on_device(acc.device):
         check(load().b2_kdk_update(n, ptr(pos), ptr(vel), acc.data_ptr(), ptr(partials), nchunks, float(h_end),
                                    float(h_begin), float(dt), phases, stream_handle(acc.device)), "kdk_update")
 
@@ -118,7 +118,7 @@ class Leapfrog:
     def _run(self, nsteps: int, init: bool = False) -> None:
         n = self.pos.shape[0]
         flags = self._flags | (_lib.B2_INIT_ACC if init else 0)
-        with torch.cuda.device(self.pos.device):
+        with on_device(self.pos.device):
             check(load().b2_leapfrog(n, self.pos.data_ptr(), self.vel.data_ptr(), self.acc.data_ptr(),
                                      float(self.eps), float(self.dt), int(nsteps), flags, self._ws.data_ptr(),
                                      self._ws.numel(), stream_handle(self.pos.device)), "leapfrog")
