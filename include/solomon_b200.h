@@ -134,10 +134,14 @@ int b2_diffusion3d_slab(int nx_local, int ny, int nz, float dx, float dy, float 
                         float kappa, const float *f, const float *halo_lo, const float *halo_hi,
                         float *fn, int i_begin, int i_end, void *stream);
 
-/* nsteps device-resident steps ping-ponging f <-> fn (no host sync). The
- * result is in fn when nsteps is odd, in f when it is even. */
+/* nsteps device-resident steps ping-ponging f <-> fn (no host sync).
+ * L2-resident grids run all steps in one cooperative launch; others one
+ * HBM pass per step (SOLOMON_DIFF_TEMPORAL=1 opts into the experimental
+ * two-steps-per-pass kernel, bit-identical to single steps).
+ * *result_in_fn (if not NULL) is set to 1 when the final field is in fn, 0
+ * when it is in f. */
 int b2_diffusion3d_run(int nx, int ny, int nz, float dx, float dy, float dz, float dt, float kappa,
-                       float *f, float *fn, int nsteps, void *stream);
+                       float *f, float *fn, int nsteps, int *result_in_fn, void *stream);
 
 #ifdef __cplusplus
 }

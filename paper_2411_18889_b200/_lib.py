@@ -46,7 +46,7 @@ SIGNATURES = {
     "b2_leapfrog_workspace_bytes": (_sz, [_i, _i]),
     "b2_diffusion3d": (_i, [_i, _i, _i, _f, _f, _f, _f, _f, _p, _p, _p]),
     "b2_diffusion3d_slab": (_i, [_i, _i, _i, _f, _f, _f, _f, _f, _p, _p, _p, _p, _i, _i, _p]),
-    "b2_diffusion3d_run": (_i, [_i, _i, _i, _f, _f, _f, _f, _f, _p, _p, _i, _p]),
+    "b2_diffusion3d_run": (_i, [_i, _i, _i, _f, _f, _f, _f, _f, _p, _p, _i, ctypes.POINTER(_i), _p]),
 }
 
 _lock = threading.Lock()

@@ -65,6 +65,30 @@ __device__ __forceinline__ float cell(const Coefs& c, float fc, float fip, float
   return v;
 }
 
+// Four consecutive-k cells at once with packed FP32 (FFMA2/FMUL2: per-lane IEEE
+// fma/mul, so identical to four cell() calls) -- halves the FP32 issue slots of
+// the stencil arithmetic. kl = f[k0-1] (clamped), kr = f[k0+4] (clamped).
+__device__ __forceinline__ float4 cell4(const Coefs& c, float4 fc, float4 fip, float4 fim, float4 fjp, float4 fjm,
+                                        float kl, float kr) {
+  const float2 ce = make_float2(c.ce, c.ce), cc = make_float2(c.cc, c.cc);
+  const float2 cn = make_float2(c.cn, c.cn), ct = make_float2(c.ct, c.ct);
+  float2 lo = __fmul2_rn(ce, make_float2(fip.x, fip.y));
+  float2 hi = __fmul2_rn(ce, make_float2(fip.z, fip.w));
+  lo = __ffma2_rn(cc, make_float2(fc.x, fc.y), lo);
+  hi = __ffma2_rn(cc, make_float2(fc.z, fc.w), hi);
+  lo = __ffma2_rn(ce, make_float2(fim.x, fim.y), lo);
+  hi = __ffma2_rn(ce, make_float2(fim.z, fim.w), hi);
+  lo = __ffma2_rn(cn, make_float2(fjp.x, fjp.y), lo);
+  hi = __ffma2_rn(cn, make_float2(fjp.z, fjp.w), hi);
+  lo = __ffma2_rn(cn, make_float2(fjm.x, fjm.y), lo);
+  hi = __ffma2_rn(cn, make_float2(fjm.z, fjm.w), hi);
+  lo = __ffma2_rn(ct, make_float2(fc.y, fc.z), lo);  // f[k+1]
+  hi = __ffma2_rn(ct, make_float2(fc.w, kr), hi);
+  lo = __ffma2_rn(ct, make_float2(kl, fc.x), lo);    // f[k-1]
+  hi = __ffma2_rn(ct, make_float2(fc.y, fc.z), hi);
+  return make_float4(lo.x, lo.y, hi.x, hi.y);
+}
+
 // ---- PTX helpers: mbarrier + bulk async copy (sm_90+/sm_100a) -------------
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -216,11 +240,7 @@ __global__ void __launch_bounds__(kMarchThreads, (S <= 2 ? 4 : 2)) k_diffusion_m
       const float kl = c4 > 0 ? rowp[4 * c4 - 1] : fcv.x;         // IMAX(k-1, 0)
       const float kr = c4 + 1 < nz4 ? rowp[4 * c4 + 4] : fcv.w;   // IMIN(k+1, nz-1)
       const float4 fm = fim[s];
-      float4 o;
-      o.x = cell(c, fcv.x, fip.x, fm.x, fjp.x, fjm.x, fcv.y, kl);
-      o.y = cell(c, fcv.y, fip.y, fm.y, fjp.y, fjm.y, fcv.z, fcv.x);
-      o.z = cell(c, fcv.z, fip.z, fm.z, fjp.z, fjm.z, fcv.w, fcv.y);
-      o.w = cell(c, fcv.w, fip.w, fm.w, fjp.w, fjm.w, kr, fcv.z);
+      const float4 o = cell4(c, fcv, fip, fm, fjp, fjm, kl, kr);
       st_stream(reinterpret_cast<float4*>(a.fn + static_cast<size_t>(p) * plane + static_cast<size_t>(j) * nz) + c4, o);
       fim[s] = fcv;
       fc[s] = fip;
@@ -229,6 +249,205 @@ __global__ void __launch_bounds__(kMarchThreads, (S <= 2 ? 4 : 2)) k_diffusion_m
     if (threadIdx.x == 0 && q + NST < L) {
       fence_proxy_async();
       issue(q + NST);
+    }
+  }
+}
+
+
+// ---------------------------------------------------------------------------
+// Two steps per HBM pass (temporal blocking) for the device-resident time
+// loop (b2_diffusion3d_run). The CTA owns output rows [j0, j0+TJ) of step 2,
+// computes step 1 on the halo-extended rows [j0-1, j0+TJ] (recomputing one row
+// on each side that the neighbour tile also computes) from input rows
+// [j0-2, j0+TJ+1] fetched by cp.async.bulk, and marches along i as a
+// wavefront: once step-1 plane q is in shared memory, step-2 plane q-1 is
+// complete. f is read once and f'' written once: 8 B per 2 cell-updates.
+// Every cell of both steps uses the same arithmetic as k_diffusion_march and
+// the same clamps (step 2 clamps onto step-1 values), so two passes of the
+// 1-step kernel and one pass of this kernel are bit-identical.
+struct March2Args {
+  const float* f;
+  float* fn;
+  int nx, ny, nz;
+  int TJ, n_jtiles, IC, nst;
+  Coefs c;
+};
+
+template <int S1, int S2>
+__global__ void __launch_bounds__(kMarchThreads, 2) k_diffusion_march2(const March2Args a) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const int nz = a.nz, ny = a.ny, nx = a.nx;
+  const int nz4 = nz >> 2;
+  const int TJ = a.TJ, NST = a.nst;
+  const size_t plane = static_cast<size_t>(ny) * nz;
+  const int in_floats = (TJ + 4) * nz;
+  const int s1_floats = (TJ + 2) * nz;
+
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw);
+  float* in_ring = reinterpret_cast<float*>(smem_raw + 128);
+  float* s1_ring = in_ring + static_cast<size_t>(NST) * in_floats;
+
+  const int jt = blockIdx.x % a.n_jtiles;
+  const int ic = blockIdx.x / a.n_jtiles;
+  const int j0 = jt * TJ;
+  const int rows = min(TJ, ny - j0);
+  const int i0 = ic * a.IC;
+  const int i1 = min(i0 + a.IC, nx);
+  if (i0 >= i1) return;
+  const int qlo = max(i0 - 1, 0), qhi = min(i1, nx - 1);   // step-1 planes
+  const int lo_in = max(qlo - 1, 0), hi_in = min(qhi + 1, nx - 1);  // input planes
+  const int L = hi_in - lo_in + 1;
+
+  const int jlo = max(j0 - 2, 0);
+  const int jhi = min(j0 + rows + 1, ny - 1);
+  const uint32_t bytes = static_cast<uint32_t>((jhi - jlo + 1) * nz * sizeof(float));
+  const int dst_row = jlo - (j0 - 2);
+
+  auto issue = [&](int t) {
+    const int st = t % NST;
+    mbar_expect_tx(bars + st, bytes);
+    bulk_g2s(in_ring + static_cast<size_t>(st) * in_floats + dst_row * nz,
+             a.f + static_cast<size_t>(lo_in + t) * plane + static_cast<size_t>(jlo) * nz, bytes, bars + st);
+  };
+  if (threadIdx.x == 0) {
+    for (int st = 0; st < NST; ++st) mbar_init(bars + st, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    for (int t = 0; t < min(NST, L); ++t) issue(t);
+  }
+  __syncthreads();
+  int next_issue = min(NST, L);  // meaningful in thread 0 only
+
+  auto in_buf = [&](int pl) -> const float* { return in_ring + static_cast<size_t>((pl - lo_in) % NST) * in_floats; };
+  auto wait_pl = [&](int pl) { const int t = pl - lo_in; mbar_wait(bars + (t % NST), (t / NST) & 1); };
+  auto s1_buf = [&](int pl) -> float* { return s1_ring + static_cast<size_t>(pl % 3) * s1_floats; };
+
+  // Positions: thread t owns column cw = t % nz4 of rows rw + s*RS (RS = 256/nz4;
+  // the planner guarantees nz4 divides 256), for s < S1 (step 1, rows of the
+  // extended tile, global row j0-1+r) and s < S2 (step 2, global row j0+r).
+  const int cw = threadIdx.x % nz4;
+  const int rw = threadIdx.x / nz4;
+  const int RS = kMarchThreads / nz4;
+  auto v1 = [&](int s) {
+    const int r = rw + s * RS;
+    const int g = j0 - 1 + r;
+    return r < TJ + 2 && g >= 0 && g < ny && g <= j0 + rows;
+  };
+  auto v2 = [&](int s) { return rw + s * RS < rows; };
+  auto in_own = [&](const float* buf, int s) -> float4 {
+    return *reinterpret_cast<const float4*>(buf + (rw + s * RS + 1) * nz + 4 * cw);
+  };
+  auto s1_own = [&](const float* buf, int s) -> float4 {
+    return *reinterpret_cast<const float4*>(buf + (rw + s * RS + 1) * nz + 4 * cw);
+  };
+
+  float4 xp[S1], xc[S1];
+  if (qlo > 0) {
+    wait_pl(qlo - 1);
+#pragma unroll
+    for (int s = 0; s < S1; ++s)
+      if (v1(s)) xp[s] = in_own(in_buf(qlo - 1), s);
+  }
+  wait_pl(qlo);
+#pragma unroll
+  for (int s = 0; s < S1; ++s)
+    if (v1(s)) {
+      xc[s] = in_own(in_buf(qlo), s);
+      if (qlo == 0) xp[s] = xc[s];
+    }
+
+  float4 ya[S2], yb[S2];
+  const Coefs c = a.c;
+
+  for (int q = qlo; q <= qhi; ++q) {
+    // ---- step 1: s1[q] on the extended tile ----
+    const float* cur = in_buf(q);
+    const bool has_next = q + 1 <= nx - 1;
+    if (has_next) wait_pl(q + 1);
+    const float* nxt = has_next ? in_buf(q + 1) : cur;
+    float* s1o = s1_buf(q);
+#pragma unroll
+    for (int s = 0; s < S1; ++s) {
+      if (!v1(s)) continue;
+      const int g = j0 - 1 + rw + s * RS;
+      const int cc4 = cw;
+      const float4 xn = has_next ? in_own(nxt, s) : xc[s];
+      const int rjp = min(g + 1, ny - 1) - (j0 - 2);
+      const int rjm = max(g - 1, 0) - (j0 - 2);
+      const float4 fjp = *reinterpret_cast<const float4*>(cur + rjp * nz + 4 * cc4);
+      const float4 fjm = *reinterpret_cast<const float4*>(cur + rjm * nz + 4 * cc4);
+      const float* rowp = cur + (g - (j0 - 2)) * nz;
+      const float4 fc = xc[s];
+      const float kl = cc4 > 0 ? rowp[4 * cc4 - 1] : fc.x;
+      const float kr = cc4 + 1 < nz4 ? rowp[4 * cc4 + 4] : fc.w;
+      const float4 fm = xp[s];
+      const float4 o = cell4(c, fc, xn, fm, fjp, fjm, kl, kr);
+      *reinterpret_cast<float4*>(s1o + (g - (j0 - 1)) * nz + 4 * cc4) = o;
+      xp[s] = fc;
+      xc[s] = xn;
+    }
+    __syncthreads();  // s1[q] complete; input planes <= q are free
+    if (threadIdx.x == 0) {
+      while (next_issue < L && next_issue - NST < q - lo_in + 1) {
+        fence_proxy_async();
+        issue(next_issue++);
+      }
+    }
+    // ---- step 2: output plane p = q-1 from s1[p-1], s1[p], s1[q] ----
+    // register queue (ya, yb) = own cells of (s1[q-2], s1[q-1])
+    const float* s1q = s1_buf(q);
+    const int p = q - 1;
+    const bool emit = p >= i0 && p < i1;
+    const float* s1p = s1_buf(p < 0 ? 0 : p);
+#pragma unroll
+    for (int s = 0; s < S2; ++s) {
+      if (!v2(s)) continue;
+      const float4 yn = s1_own(s1q, s);
+      if (q == 0) {  // IMAX(p-1, 0): s1[-1] is s1[0]
+        ya[s] = yn;
+        yb[s] = yn;
+        continue;
+      }
+      if (emit) {
+        const int g = j0 + rw + s * RS;
+        const int cc4 = cw;
+        const int rjp = min(g + 1, ny - 1) - (j0 - 1);
+        const int rjm = max(g - 1, 0) - (j0 - 1);
+        const float4 fjp = *reinterpret_cast<const float4*>(s1p + rjp * nz + 4 * cc4);
+        const float4 fjm = *reinterpret_cast<const float4*>(s1p + rjm * nz + 4 * cc4);
+        const float* rowp = s1p + (g - (j0 - 1)) * nz;
+        const float4 fc = yb[s];
+        const float kl = cc4 > 0 ? rowp[4 * cc4 - 1] : fc.x;
+        const float kr = cc4 + 1 < nz4 ? rowp[4 * cc4 + 4] : fc.w;
+        const float4 fm = ya[s];
+        const float4 o = cell4(c, fc, yn, fm, fjp, fjm, kl, kr);
+        st_stream(
+            reinterpret_cast<float4*>(a.fn + static_cast<size_t>(p) * plane + static_cast<size_t>(g) * nz) + cc4, o);
+      }
+      ya[s] = yb[s];
+      yb[s] = yn;
+    }
+  }
+  // Last output plane at the global upper boundary: next = IMIN(p+1, nx-1) = p.
+  if (i1 == nx) {
+    const int p = nx - 1;
+    const float* s1p = s1_buf(p);
+#pragma unroll
+    for (int s = 0; s < S2; ++s) {
+      if (!v2(s)) continue;
+      const int g = j0 + rw + s * RS;
+      const int cc4 = cw;
+      const int rjp = min(g + 1, ny - 1) - (j0 - 1);
+      const int rjm = max(g - 1, 0) - (j0 - 1);
+      const float4 fjp = *reinterpret_cast<const float4*>(s1p + rjp * nz + 4 * cc4);
+      const float4 fjm = *reinterpret_cast<const float4*>(s1p + rjm * nz + 4 * cc4);
+      const float* rowp = s1p + (g - (j0 - 1)) * nz;
+      const float4 fc = yb[s];
+      const float kl = cc4 > 0 ? rowp[4 * cc4 - 1] : fc.x;
+      const float kr = cc4 + 1 < nz4 ? rowp[4 * cc4 + 4] : fc.w;
+      const float4 fm = ya[s];
+      const float4 o = cell4(c, fc, fc, fm, fjp, fjm, kl, kr);
+      st_stream(reinterpret_cast<float4*>(a.fn + static_cast<size_t>(p) * plane + static_cast<size_t>(g) * nz) + cc4,
+                o);
     }
   }
 }
@@ -291,11 +510,7 @@ __global__ void __launch_bounds__(256)
     const float4 fjm = __ldg(reinterpret_cast<const float4*>(P + static_cast<size_t>(max(j - 1, 0)) * nz + 4 * c4));
     const float kl = c4 > 0 ? __ldg(P + jk - 1) : fc.x;
     const float kr = c4 + 1 < nz4 ? __ldg(P + jk + 4) : fc.w;
-    float4 o;
-    o.x = cell(c, fc.x, fip.x, fim.x, fjp.x, fjm.x, fc.y, kl);
-    o.y = cell(c, fc.y, fip.y, fim.y, fjp.y, fjm.y, fc.z, fc.x);
-    o.z = cell(c, fc.z, fip.z, fim.z, fjp.z, fjm.z, fc.w, fc.y);
-    o.w = cell(c, fc.w, fip.w, fim.w, fjp.w, fjm.w, kr, fc.z);
+    const float4 o = cell4(c, fc, fip, fim, fjp, fjm, kl, kr);
     *reinterpret_cast<float4*>(fn + static_cast<size_t>(i) * plane + jk) = o;
   }
 }
@@ -332,11 +547,7 @@ __global__ void __launch_bounds__(256)
       const float4 fjm = *reinterpret_cast<const float4*>(P + static_cast<size_t>(max(j - 1, 0)) * nz + 4 * c4);
       const float kl = c4 > 0 ? P[jk - 1] : fc.x;
       const float kr = c4 + 1 < nz4 ? P[jk + 4] : fc.w;
-      float4 o;
-      o.x = cell(c, fc.x, fip.x, fim.x, fjp.x, fjm.x, fc.y, kl);
-      o.y = cell(c, fc.y, fip.y, fim.y, fjp.y, fjm.y, fc.z, fc.x);
-      o.z = cell(c, fc.z, fip.z, fim.z, fjp.z, fjm.z, fc.w, fc.y);
-      o.w = cell(c, fc.w, fip.w, fim.w, fjp.w, fjm.w, kr, fc.z);
+      const float4 o = cell4(c, fc, fip, fim, fjp, fjm, kl, kr);
       *reinterpret_cast<float4*>(fn + static_cast<size_t>(i) * plane + jk) = o;
     }
     grid.sync();
@@ -391,6 +602,63 @@ static bool plan_march(int nx_out, int ny, int nz, MarchPlan& mp) {
   mp.IC = (nx_out + splits - 1) / splits;
   mp.grid = mp.n_jtiles * ((nx_out + mp.IC - 1) / mp.IC);
   return true;
+}
+
+// Temporal-blocked (2 steps per pass) plan: S1 = 4 (or 8) step-1 float4 cells per
+// thread on TJ+2 rows, S2 <= 4 step-2 cells on TJ rows; 3-stage input ring +
+// 3-plane step-1 ring in shared memory, two CTAs per SM.
+struct March2Plan {
+  int S1 = 0, S2 = 0, TJ = 0, nst = 3, n_jtiles = 0, IC = 0, grid = 0;
+  size_t smem = 0;
+};
+
+static bool plan_march2(int nx, int ny, int nz, March2Plan& mp) {
+  if (nz % 4 != 0) return false;
+  const int nz4 = nz / 4;
+  if (nz4 > kMarchThreads || kMarchThreads % nz4 != 0) return false;  // positions: rw + s * (256 / nz4)
+  const DeviceInfo& di = device_info();
+  static const int force_tj = env_int("SOLOMON_DIFF_TB_TJ", 0);
+  const int S1 = 4;
+  int TJ = (kMarchThreads * S1) / nz4 - 2;
+  if (force_tj) TJ = std::min(TJ, force_tj);
+  TJ = std::min(TJ, ny);
+  if (TJ < 1) return false;
+  const int S2 = (TJ * nz4 + kMarchThreads - 1) / kMarchThreads;
+  if (S2 > 4) return false;
+  const size_t smem = 128 + static_cast<size_t>(mp.nst) * (TJ + 4) * nz * 4 + 3ull * (TJ + 2) * nz * 4;
+  if (smem > (228 * 1024) / 2 - 1024) return false;
+  mp.S1 = S1;
+  mp.S2 = S2 <= 3 ? 3 : 4;
+  mp.TJ = TJ;
+  mp.smem = smem;
+  (void)di;
+  mp.n_jtiles = (ny + mp.TJ - 1) / mp.TJ;
+  const int resident = 2 * device_info().sms;
+  int splits = std::max(1, resident / mp.n_jtiles);
+  splits = std::min(splits, std::max(1, nx / 8));
+  mp.IC = (nx + splits - 1) / splits;
+  mp.grid = mp.n_jtiles * ((nx + mp.IC - 1) / mp.IC);
+  return true;
+}
+
+template <int S1, int S2>
+static void launch_march2_t(const March2Plan& mp, const March2Args& a, cudaStream_t s) {
+  static bool set = false;
+  if (!set) {
+    cudaFuncSetAttribute(k_diffusion_march2<S1, S2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    set = true;
+  }
+  k_diffusion_march2<S1, S2><<<mp.grid, kMarchThreads, mp.smem, s>>>(a);
+}
+
+static int launch_march2(const March2Plan& mp, int nx, int ny, int nz, const Coefs& c, const float* f, float* fn,
+                         cudaStream_t s) {
+  March2Args a{f, fn, nx, ny, nz, mp.TJ, mp.n_jtiles, mp.IC, mp.nst, c};
+  if (mp.S2 == 3)
+    launch_march2_t<4, 3>(mp, a, s);
+  else
+    launch_march2_t<4, 4>(mp, a, s);
+  return launch_status();
 }
 
 static int launch_step(int nx, int ny, int nz, const Coefs& c, const float* f, const float* lo, const float* hi,
@@ -465,15 +733,21 @@ int b2_diffusion3d_slab(int nx_local, int ny, int nz, float dx, float dy, float 
 }
 
 int b2_diffusion3d_run(int nx, int ny, int nz, float dx, float dy, float dz, float dt, float kappa, float* f,
-                       float* fn, int nsteps, void* stream) {
+                       float* fn, int nsteps, int* result_in_fn, void* stream) {
   if (int rc = check_grid(nx, ny, nz, f, fn)) return rc;
   if (nsteps < 0) return B2_EINVAL;
   const Coefs c = make_coefs(dx, dy, dz, dt, kappa);
   cudaStream_t s = as_stream(stream);
+  if (result_in_fn) *result_in_fn = nsteps & 1;
   static const long long direct_max = env_int("SOLOMON_DIFF_DIRECT_MAXCELLS", 1 << 22);
   static const int use_multi = env_int("SOLOMON_DIFF_MULTI", 1);
+  // Temporal blocking is opt-in: on B200 the 2-step kernel is latency/issue-bound
+  // at 16 warps/SM (716 vs 790 GLUPS at 512^3), so one step per
+  // pass -- already at 97% of copy bandwidth -- stays the default.
+  static const int use_tb = env_int("SOLOMON_DIFF_TEMPORAL", 0);
   const long long cells = static_cast<long long>(nx) * ny * nz;
-  if (use_multi && nsteps > 1 && nz % 4 == 0 && aligned16(f) && aligned16(fn) && cells <= direct_max) {
+  const bool aligned = nz % 4 == 0 && aligned16(f) && aligned16(fn);
+  if (use_multi && nsteps > 1 && aligned && cells <= direct_max) {
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_diffusion_multi, 256, 0);
     const long long work = (cells / 4 + 255) / 256;
@@ -490,10 +764,19 @@ int b2_diffusion3d_run(int nx, int ny, int nz, float dx, float dy, float dz, flo
   }
   float* a = f;
   float* b = fn;
-  for (int st = 0; st < nsteps; ++st) {
+  int done = 0;
+  March2Plan m2;
+  if (use_tb && nsteps >= 2 && aligned && plan_march2(nx, ny, nz, m2)) {
+    for (; done + 2 <= nsteps; done += 2) {
+      if (int rc = launch_march2(m2, nx, ny, nz, c, a, b, s)) return rc;
+      std::swap(a, b);
+    }
+  }
+  for (; done < nsteps; ++done) {
     if (int rc = launch_step(nx, ny, nz, c, a, nullptr, nullptr, b, 0, nx, s)) return rc;
     std::swap(a, b);
   }
+  if (result_in_fn) *result_in_fn = a == fn;
   return B2_OK;
 }
 

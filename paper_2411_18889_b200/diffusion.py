@@ -11,6 +11,7 @@ tensors as ``f`` / ``fn``; it runs the sm_100a marching kernel in
 """
 from __future__ import annotations
 
+import ctypes
 from dataclasses import dataclass, field
 
 import torch
@@ -102,12 +103,14 @@ class Diffusion3D:
         return self.f
 
     def run(self, nsteps: int) -> torch.Tensor:
+        """Advance ``nsteps`` (b2_diffusion3d_run: two steps per HBM pass on large grids)."""
         nx, ny, nz = self.f.shape
+        in_fn = ctypes.c_int(0)
         with on_device(self.f.device):
             check(load().b2_diffusion3d_run(nx, ny, nz, self.dx, self.dy, self.dz, self.dt, self.kappa,
-                                            self.f.data_ptr(), self._fn.data_ptr(), int(nsteps),
+                                            self.f.data_ptr(), self._fn.data_ptr(), int(nsteps), ctypes.byref(in_fn),
                                             stream_handle(self.f.device)), "diffusion3d_run")
-        if nsteps % 2:
+        if in_fn.value:
             self.f, self._fn = self._fn, self.f
         return self.f
 

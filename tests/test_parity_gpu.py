@@ -287,3 +287,38 @@ def test_residency_helpers_present_contract(b2, golden):
     assert not R.is_present(f0) and not R.is_present(fn)
     with pytest.raises(b2.SolomonError):
         R.present(f0)
+
+
+@pytest.mark.parametrize("shape,steps", [((40, 37, 128), 2), ((40, 37, 128), 5), ((13, 9, 512), 4),
+                                         ((256, 64, 512), 6), ((300, 70, 256), 3), ((66, 130, 1024), 2),
+                                         ((5, 3, 2048), 4), ((1, 7, 64), 2), ((2, 1, 512), 4), ((64, 64, 100), 4)])
+def test_diffusion_run_temporal_blocking_bit_identical(b2, restatement, shape, steps, monkeypatch):
+    """b2_diffusion3d_run (2 steps per HBM pass + remainder) == sequential single steps, bit for bit."""
+    args = (0.03, 0.02, 0.025, 2e-5, 1.0)
+    f0 = np.random.default_rng(11).random(shape, dtype=np.float32)
+    want = restatement.diffusion_run(f0, steps, *args)
+    sim = b2.Diffusion3D(dev(f0), *args)
+    got = sim.run(steps).cpu().numpy()
+    assert bits_equal(got, want)
+
+
+def test_temporal_blocking_kernel_opt_in_bit_identical(tmp_path):
+    """The opt-in 2-steps-per-pass kernel (SOLOMON_DIFF_TEMPORAL=1) in a fresh process."""
+    import os
+    import subprocess
+    import sys
+
+    code = (
+        "import sys, numpy as np, torch; sys.path.insert(0, '.'); sys.path.insert(0, 'tests')\n"
+        "import oracle, paper_2411_18889_b200 as b2\n"
+        "args = (0.03, 0.02, 0.025, 2e-5, 1.0)\n"
+        "for shape, steps in [((40, 37, 128), 4), ((13, 9, 512), 5), ((256, 64, 512), 6), ((66, 30, 1024), 2)]:\n"
+        "    f0 = np.random.default_rng(3).random(shape, dtype=np.float32)\n"
+        "    want = oracle.Restatement().diffusion_run(f0, steps, *args)\n"
+        "    got = b2.Diffusion3D(torch.from_numpy(f0).cuda(), *args).run(steps).cpu().numpy()\n"
+        "    assert np.array_equal(got.view(np.uint32), want.view(np.uint32)), shape\n"
+        "print('ok')\n")
+    env = dict(os.environ, SOLOMON_DIFF_TEMPORAL="1", SOLOMON_DIFF_DIRECT_MAXCELLS="0")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True)
+    assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-2000:]
