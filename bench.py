@@ -52,6 +52,8 @@ def parse_args():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-diffusion", action="store_true")
     ap.add_argument("--no-configs", action="store_true", help="skip the BASELINE parity configs [0] and [1]")
+    ap.add_argument("--dist", action="store_true",
+                    help="use the multi-GPU drivers (NCCL) even at world size 1 (smoke-tests the N>1 path)")
     ap.add_argument("--cpu-seconds", type=float, default=8.0, help="target CPU time per baseline sample")
     return ap.parse_args()
 
@@ -268,9 +270,10 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     fp32_peak = probe.solomon_probe_fp32_tflops(5)
 
     # ---------------- N-body ----------------
+    sharded = world > 1 or args.dist
     n = args.n or ((1 << 20) if world == 1 else (1 << 22))
     pos_np, vel_np = b2.plummer_numpy(n, 42)
-    if world == 1:
+    if not sharded:
         pos = torch.from_numpy(pos_np).to(dev)
         vel = torch.from_numpy(vel_np).to(dev)
         nch = lib.b2_calc_acc_nchunks(n, 0)
@@ -342,10 +345,10 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     barrier()
     clock_rec = clocks.stop() if clocks else None
     step_ms = [e[0].elapsed_time(e[2]) for e in events]
-    force_ms = [(e[3] if world > 1 else e[0]).elapsed_time(e[1]) for e in events]
+    force_ms = [(e[3] if sharded else e[0]).elapsed_time(e[1]) for e in events]
     total_ms = max_over_ranks(sum(step_ms))
     force_avg = max_over_ranks(statistics.mean(force_ms))
-    gather_ms = max_over_ranks(statistics.mean(e[0].elapsed_time(e[3]) for e in events)) if world > 1 else 0.0
+    gather_ms = max_over_ranks(statistics.mean(e[0].elapsed_time(e[3]) for e in events)) if sharded else 0.0
     interactions = float(n) * float(n)
     value = interactions * args.steps / (total_ms * 1e-3) / 1e9
     achieved_tf = FLOP_PER_INTERACTION * float(n_local) * float(n) / (force_avg * 1e-3) / 1e12
@@ -431,7 +434,8 @@ def run_diffusion(args, rank, world, dev, stream, peaks, barrier, max_over_ranks
     g = args.grid or (512 if world == 1 else 1024)
     dx = 1.0 / g
     dargs = (dx, dx, dx, 0.1 * dx * dx, 1.0)
-    if world == 1:
+    single = world == 1 and not args.dist
+    if single:
         f = b2.init_grid(g, g, g, seed=7, device=dev)
         fn = torch.empty_like(f)
         bufs = [f, fn]
@@ -472,7 +476,7 @@ def run_diffusion(args, rank, world, dev, stream, peaks, barrier, max_over_ranks
     out = {
         "metric": "diffusion GLUPS", "value": glups, "unit": "GLUPS", "ms_per_step": step_ms,
         "steps": args.dsteps, "warmup": 5, "dtype": "f32",
-        "config": {"workload": f"diffusion3d {g}^3 FP32 7-point step" + (" (single GPU)" if world == 1 else
+        "config": {"workload": f"diffusion3d {g}^3 FP32 7-point step" + (" (single GPU)" if launches == 1 else
                                                                           f", i-slabs x{world} + NCCL halo"),
                    "grid": [g, g, g], "dt_over_dx2": 0.1,
                    "l2": "inputs (2 x {:.0f} MiB per GPU) larger than L2; no flush".format(4 * nxl * g * g / 2**20)},
@@ -482,7 +486,7 @@ def run_diffusion(args, rank, world, dev, stream, peaks, barrier, max_over_ranks
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "_source" not in peaks else peaks["_source"]},
         "gpu_launches": launches * args.dsteps,
     }
-    if world == 1:
+    if single:
         host_f = f.cpu().pin_memory()
         host_fn = torch.empty_like(host_f).pin_memory()
         P = ctypes.c_void_p
@@ -594,16 +598,18 @@ def main():
         if out is not None:
             print(json.dumps(out), flush=True)
         return
-    if world > 1:
+    if world > 1 or args.dist:
         import torch
         import torch.distributed as dist
 
         torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29511")
+        dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", local_rank))
     out = run_ours(args, rank, world, local_rank)
     if rank == 0:
         print(json.dumps(out), flush=True)
-    if world > 1:
+    if world > 1 or args.dist:
         import torch.distributed as dist
 
         dist.barrier()
