@@ -1,0 +1,52 @@
+"""CPU: bench.py's reference arm (no GPU needed) prints one well-formed JSON line."""
+from __future__ import annotations
+
+import json
+import pathlib
+import subprocess
+import sys
+
+import pytest
+
+ROOT = pathlib.Path(__file__).resolve().parents[1]
+
+
+def test_reference_arm_json_line():
+    import oracle
+
+    if not oracle.Reference.available("fast"):
+        pytest.skip("oracle/_ref not built")
+    out = subprocess.run([sys.executable, "bench.py", "--impl", "reference", "--steps", "1", "--warmup", "0",
+                          "--cpu-seconds", "0.3", "--n", "16384", "--grid", "64"],
+                         cwd=ROOT, capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.strip()]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["impl"] == "reference" and d["unit"] == "Ginteractions/s" and d["value"] > 0
+    assert d["cpu_baseline"]["kind"] == "reference" and d["cpu_baseline"]["cores"] >= 1
+    assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["value"] == d["value"]
+    assert d["secondary"]["diffusion"]["value"] > 0
+
+
+def test_clock_sampler_parses_nvidia_smi_csv(tmp_path):
+    sys.path.insert(0, str(ROOT))
+    import bench
+
+    s = bench.ClockSampler(0)
+    s.file = open(tmp_path / "c.csv", "w+")
+    s.file.write("0, 1965, 1965, 700.1, 0x0, Not Active, Not Active, Not Active, Not Active\n"
+                 "0, 1800, 1965, 990.0, 0x4, Not Active, Not Active, Not Active, Active\n"
+                 "0, 1965, 1965, 800.0, 0x0, Not Active, Not Active, Not Active, Not Active\n")
+    s.file.flush()
+
+    class _P:
+        def terminate(self):
+            pass
+
+        def wait(self, timeout=None):
+            return 0
+
+    s.proc = _P()
+    rec = s.stop()
+    assert rec == {"sm_mhz": 1965.0, "sm_max_mhz": 1965.0, "reasons": ["sw_power_cap"], "samples": 3}

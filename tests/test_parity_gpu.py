@@ -322,3 +322,51 @@ def test_temporal_blocking_kernel_opt_in_bit_identical(tmp_path):
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     out = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True)
     assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-2000:]
+
+
+def test_dropin_edge_cases(b2, golden, restatement):
+    """Ni != Nj on host pointers, Nj = 0 (zero acceleration), Ni = 0 (no-op)."""
+    lib = b2.load()
+    ipos = np.ascontiguousarray(golden["nbody/subset/ipos"])
+    jpos = np.ascontiguousarray(golden["nbody/subset/jpos"])
+    eps = float(golden["nbody/subset/eps"])
+    out = np.zeros_like(ipos)
+    lib.calc_acc(len(ipos), _cptr(ipos), _cptr(out), len(jpos), _cptr(jpos), eps)
+    assert lib.b2_last_error() == 0
+    assert rel_l2(out, golden["nbody/subset/acc"]) <= TOL_ACC
+    out[:] = 7.0
+    lib.calc_acc(len(ipos), _cptr(ipos), _cptr(out), 0, _cptr(jpos), eps)
+    assert lib.b2_last_error() == 0 and np.all(out == 0)
+    out[:] = 7.0
+    lib.calc_acc(0, _cptr(ipos), _cptr(out), len(jpos), _cptr(jpos), eps)
+    assert lib.b2_last_error() == 0 and np.all(out == 7.0)
+
+
+def test_stream_ordering_on_side_stream(b2, restatement):
+    """Calls are ordered on torch's current stream (here a side stream), not the default stream."""
+    pos, _ = b2.plummer_numpy(4096, 5)
+    f0 = np.random.default_rng(1).random((32, 48, 64), dtype=np.float32)
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        p = dev(pos)
+        acc = b2.accelerations(p, 2.0 ** -6)
+        f = dev(f0)
+        fn = torch.empty_like(f)
+        b2.diffusion3d(32, 48, 64, 0.1, 0.1, 0.1, 1e-3, 1.0, f, fn)
+    s.synchronize()
+    assert rel_l2(acc.cpu().numpy(), restatement.calc_acc(pos, pos, 2.0 ** -6)) <= TOL_ACC
+    assert bits_equal(fn.cpu().numpy(), restatement.diffusion3d(f0, 0.1, 0.1, 0.1, 1e-3, 1.0))
+
+
+def test_large_n_int_indexing(b2):
+    """N = 2^22 single-GPU force (the configs[3] total): finite, momentum-balanced (sampled)."""
+    n = 1 << 22
+    pos, _ = b2.plummer_numpy(n, 42)
+    p = dev(pos)
+    sub = p[: 1 << 12].contiguous()
+    acc = b2.accelerations(sub, 2.0 ** -6, p).cpu().numpy()
+    assert np.all(np.isfinite(acc))
+    import oracle
+
+    want = oracle.Restatement().calc_acc(pos[:256], pos, 2.0 ** -6)
+    assert rel_l2(acc[:256], want) <= 1e-4
