@@ -370,3 +370,18 @@ def test_large_n_int_indexing(b2):
 
     want = oracle.Restatement().calc_acc(pos[:256], pos, 2.0 ** -6)
     assert rel_l2(acc[:256], want) <= 1e-4
+
+
+@pytest.mark.parametrize("shape", [(64, 48, 40), (100, 33, 64), (17, 8, 12)])
+def test_dropin_diffusion_pipelined_host_path(b2, restatement, shape):
+    """Host-pointer diffusion3d drop-in: chunked H2D / stencil / D2H pipeline, bit-identical."""
+    lib = b2.load()
+    f0 = np.random.default_rng(2).random(shape, dtype=np.float32)
+    args = (0.05, 0.04, 0.03, 1e-4, 1.0)
+    want = restatement.diffusion3d(f0, *args)
+    for pinned in (False, True):
+        src = torch.from_numpy(f0).pin_memory() if pinned else torch.from_numpy(f0.copy())
+        dst = torch.empty(shape, dtype=torch.float32).pin_memory() if pinned else torch.empty(shape)
+        lib.diffusion3d(*shape, *args, ctypes.c_void_p(src.data_ptr()), ctypes.c_void_p(dst.data_ptr()))
+        assert lib.b2_last_error() == 0
+        assert bits_equal(dst.numpy(), want)
