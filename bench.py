@@ -52,6 +52,8 @@ def parse_args():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-diffusion", action="store_true")
     ap.add_argument("--no-configs", action="store_true", help="skip the BASELINE parity configs [0] and [1]")
+    ap.add_argument("--halo", choices=["p2p", "nccl"], default="p2p",
+                    help="diffusion halo transport for N>1: fused peer-memory reads (p2p) or NCCL send/recv")
     ap.add_argument("--dist", action="store_true",
                     help="use the multi-GPU drivers (NCCL) even at world size 1 (smoke-tests the N>1 path)")
     ap.add_argument("--cpu-seconds", type=float, default=8.0, help="target CPU time per baseline sample")
@@ -435,6 +437,7 @@ def run_diffusion(args, rank, world, dev, stream, peaks, barrier, max_over_ranks
     dx = 1.0 / g
     dargs = (dx, dx, dx, 0.1 * dx * dx, 1.0)
     single = world == 1 and not args.dist
+    transport = None
     if single:
         f = b2.init_grid(g, g, g, seed=7, device=dev)
         fn = torch.empty_like(f)
@@ -450,7 +453,13 @@ def run_diffusion(args, rank, world, dev, stream, peaks, barrier, max_over_ranks
         nxl = g // world
         gen = torch.Generator(device=dev).manual_seed(7 + rank)
         f_local = torch.rand((nxl, g, g), generator=gen, dtype=torch.float32, device=dev)
-        sim = SlabDiffusion(f_local, *dargs)
+        transport = args.halo
+        try:
+            sim = SlabDiffusion(f_local, *dargs, transport=transport)
+        except Exception as e:  # noqa: BLE001 -- report and fall back to the NCCL transport
+            print(f"p2p halo transport unavailable ({e}); using NCCL", file=sys.stderr)
+            transport = "nccl"
+            sim = SlabDiffusion(f_local, *dargs, transport=transport)
 
         def dstep(i):
             sim.step(1)
@@ -476,8 +485,8 @@ def run_diffusion(args, rank, world, dev, stream, peaks, barrier, max_over_ranks
     out = {
         "metric": "diffusion GLUPS", "value": glups, "unit": "GLUPS", "ms_per_step": step_ms,
         "steps": args.dsteps, "warmup": 5, "dtype": "f32",
-        "config": {"workload": f"diffusion3d {g}^3 FP32 7-point step" + (" (single GPU)" if launches == 1 else
-                                                                          f", i-slabs x{world} + NCCL halo"),
+        "config": {"workload": f"diffusion3d {g}^3 FP32 7-point step" + (
+                       " (single GPU)" if single else f", i-slabs x{world}, halo transport {transport}"),
                    "grid": [g, g, g], "dt_over_dx2": 0.1,
                    "l2": "inputs (2 x {:.0f} MiB per GPU) larger than L2; no flush".format(4 * nxl * g * g / 2**20)},
         "roofline": {"bound": "hbm", "kernel": "k_diffusion_march", "achieved": achieved,

@@ -143,6 +143,18 @@ int b2_diffusion3d_slab(int nx_local, int ny, int nz, float dx, float dy, float 
 int b2_diffusion3d_run(int nx, int ny, int nz, float dx, float dy, float dz, float dt, float kappa,
                        float *f, float *fn, int nsteps, int *result_in_fn, void *stream);
 
+/* --- Peer memory across processes (multi-GPU fused halo) --- */
+
+/* Size of an exported handle (a cudaIpcMemHandle_t, 64 bytes). */
+size_t b2_ipc_handle_bytes(void);
+/* Export the allocation holding dptr: handle (b2_ipc_handle_bytes() bytes) and
+ * dptr's offset inside that allocation. */
+int b2_ipc_export(const void *dptr, void *handle, size_t *offset);
+/* Map a peer's exported allocation into this process (peer access enabled on
+ * demand) and return the address of the exported pointer. */
+int b2_ipc_import(const void *handle, size_t offset, void **dptr);
+int b2_ipc_close(void *dptr, size_t offset);
+
 #ifdef __cplusplus
 }
 #endif

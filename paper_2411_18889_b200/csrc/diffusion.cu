@@ -669,7 +669,10 @@ static int launch_step(int nx, int ny, int nz, const Coefs& c, const float* f, c
   // Grids whose two fields sit comfortably in L2 take the direct kernel.
   static const long long direct_max = env_int("SOLOMON_DIFF_DIRECT_MAXCELLS", 1 << 22);
   const long long cells = static_cast<long long>(i_end - i_begin) * ny * nz;
-  if (ok_align && nz % 4 == 0 && cells <= direct_max) {
+  // ...and so do thin boundary launches of a slab: their halo planes may live in
+  // a peer GPU's memory (fused halo transport), read here with plain loads.
+  const bool thin_halo = (i_end - i_begin) <= 2 && (lo || hi);
+  if (ok_align && nz % 4 == 0 && (cells <= direct_max || thin_halo)) {
     const long long work = cells / 4;
     const int grid = static_cast<int>(std::min<long long>((work + 255) / 256, 148LL * 16));
     k_diffusion_direct<<<grid, 256, 0, s>>>(f, lo, hi, fn, nx, ny, nz, i_begin, i_end, c);

@@ -23,6 +23,7 @@ fails loudly without it.
 """
 from __future__ import annotations
 
+import ctypes
 from dataclasses import dataclass
 
 import torch
@@ -63,8 +64,9 @@ class CudaSlabKernels:
         self.lib = _lib.load()
 
     def slab(self, f, fn, halo_lo, halo_hi, i_begin, i_end) -> None:
+        """Halo arguments are tensors, raw device addresses (peer memory) or None."""
         nx, ny, nz = f.shape
-        ptr = lambda t: t.data_ptr() if t is not None else None  # noqa: E731
+        ptr = lambda t: t if (t is None or isinstance(t, int)) else t.data_ptr()  # noqa: E731
         _lib.check(self.lib.b2_diffusion3d_slab(nx, ny, nz, *self.args, f.data_ptr(), ptr(halo_lo), ptr(halo_hi),
                                                 fn.data_ptr(), i_begin, i_end, _lib.stream_handle(f.device)),
                    "diffusion3d_slab")
@@ -163,12 +165,29 @@ class SlabDiffusion:
     """Explicit diffusion on i-slabs with a one-plane halo exchange per step.
 
     ``f_local`` is this rank's ``[nx_local, ny, nz]`` block of the global grid
-    (planes [rank*nx_local, (rank+1)*nx_local)).
+    (planes [rank*nx_local, (rank+1)*nx_local) for equal splits; ranks may
+    differ in nx_local).
+
+    ``transport="nccl"``: the two edge planes go to the neighbours with grouped
+    NCCL send/recv on a comm stream while the interior computes.
+
+    ``transport="p2p"`` (fused halo, no collective): every rank maps its
+    neighbours' field buffers into its address space once (CUDA IPC; peer access
+    over NVLink/NVSwitch), and the boundary-plane stencil launches read the halo
+    planes directly from the neighbour's memory. Ordering is stream-side: each
+    rank records an interprocess event after its step; before the next step a
+    rank makes its stream wait on the neighbours' events (their planes are final
+    and they have finished reading ours). A CPU-only barrier on a gloo group
+    ensures those events were recorded before they are waited on; it never
+    synchronises a GPU.
     """
 
-    def __init__(self, f_local: torch.Tensor, dx, dy, dz, dt, kappa=1.0, *, group=None, kernels=None):
+    def __init__(self, f_local: torch.Tensor, dx, dy, dz, dt, kappa=1.0, *, group=None, kernels=None,
+                 transport: str = "nccl"):
         if f_local.dim() != 3 or f_local.shape[0] < 2:
             raise ValueError("f_local must be [nx_local >= 2, ny, nz]")
+        if transport not in ("nccl", "p2p"):
+            raise ValueError(f"unknown transport {transport!r}")
         self.group = group
         self.world, self.rank = dist.get_world_size(group), dist.get_rank(group)
         self.k = kernels or CudaSlabKernels(dx, dy, dz, dt, kappa)
@@ -177,11 +196,89 @@ class SlabDiffusion:
         ny, nz = self.f.shape[1:]
         self.has_lo = self.rank > 0
         self.has_hi = self.rank < self.world - 1
-        self.halo_lo = torch.empty((ny, nz), dtype=self.f.dtype, device=self.f.device) if self.has_lo else None
-        self.halo_hi = torch.empty((ny, nz), dtype=self.f.dtype, device=self.f.device) if self.has_hi else None
         self.is_cuda = self.f.is_cuda
-        self.comm = torch.cuda.Stream(device=self.f.device) if self.is_cuda else None
+        self.transport = transport
+        self.steps_done = 0
+        if transport == "nccl":
+            self.halo_lo = torch.empty((ny, nz), dtype=self.f.dtype, device=self.f.device) if self.has_lo else None
+            self.halo_hi = torch.empty((ny, nz), dtype=self.f.dtype, device=self.f.device) if self.has_hi else None
+            self.comm = torch.cuda.Stream(device=self.f.device) if self.is_cuda else None
+        else:
+            if not self.is_cuda:
+                raise ValueError("transport='p2p' needs CUDA tensors")
+            self._setup_p2p()
 
+    # ---- p2p transport -------------------------------------------------------
+    def _setup_p2p(self) -> None:
+        lib = _lib.load()
+        self.ctrl = dist.new_group(backend="gloo") if dist.get_backend(self.group) != "gloo" else self.group
+        hb = lib.b2_ipc_handle_bytes()
+        bufs = (self.f, self.fn)  # buffer k holds f_s for s % 2 == k on every rank
+        mine = []
+        for t in bufs:
+            h = ctypes.create_string_buffer(hb)
+            off = ctypes.c_size_t(0)
+            _lib.check(lib.b2_ipc_export(t.data_ptr(), h, ctypes.byref(off)), "ipc_export")
+            mine.append((h.raw, off.value))
+        self.event = torch.cuda.Event(enable_timing=False, interprocess=True)
+        self.event.record(torch.cuda.current_stream(self.f.device))
+        info = {"bufs": mine, "nxl": self.f.shape[0], "event": bytes(self.event.ipc_handle())}
+        everyone = [None] * self.world
+        dist.all_gather_object(everyone, info, group=self.ctrl)
+        self._peer = {}  # rank -> (nxl, [ptr0, ptr1], [(ptr, off)], event)
+        err = None
+        try:
+            for r in (self.rank - 1, self.rank + 1):
+                if 0 <= r < self.world:
+                    ptrs, opened = [], []
+                    for h, off in everyone[r]["bufs"]:
+                        p = ctypes.c_void_p()
+                        _lib.check(lib.b2_ipc_import(ctypes.create_string_buffer(h, len(h)), off, ctypes.byref(p)),
+                                   "ipc_import")
+                        ptrs.append(p.value)
+                        opened.append((p.value, off))
+                    ev = torch.cuda.Event.from_ipc_handle(self.f.device, everyone[r]["event"])
+                    self._peer[r] = (everyone[r]["nxl"], ptrs, opened, ev)
+        except Exception as e:  # noqa: BLE001 -- agreed on below so that no rank is left in a collective
+            err = e
+        ok = torch.tensor([0 if err else 1], dtype=torch.int32)
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN, group=self.ctrl)
+        if not int(ok.item()):
+            for _, _, opened, _ in self._peer.values():
+                for p, off in opened:
+                    lib.b2_ipc_close(p, off)
+            self._peer = {}
+            raise _lib.SolomonError(f"p2p halo transport unavailable on some rank: {err or 'peer failure'}")
+        torch.cuda.synchronize(self.f.device)  # f_0 complete everywhere before anyone reads it
+        dist.barrier(group=self.ctrl)
+
+    def _halo_ptrs(self):
+        """Peer addresses of the neighbours' edge planes of f_s (s = steps_done)."""
+        ny, nz = self.f.shape[1:]
+        plane_bytes = ny * nz * self.f.element_size()
+        par = self.steps_done % 2
+        lo = hi = None
+        if self.has_lo:
+            nxl, ptrs, _, _ = self._peer[self.rank - 1]
+            lo = ptrs[par] + (nxl - 1) * plane_bytes
+        if self.has_hi:
+            _, ptrs, _, _ = self._peer[self.rank + 1]
+            hi = ptrs[par]
+        return lo, hi
+
+    def close(self) -> None:
+        if self.transport != "p2p" or not getattr(self, "_peer", None):
+            return
+        torch.cuda.synchronize(self.f.device)
+        dist.barrier(group=self.ctrl)
+        lib = _lib.load()
+        for _, _, opened, _ in self._peer.values():
+            for p, off in opened:
+                lib.b2_ipc_close(p, off)
+        self._peer = {}
+        dist.barrier(group=self.ctrl)
+
+    # ---- stepping --------------------------------------------------------------
     def _exchange_ops(self):
         ops = []
         g = self.group
@@ -193,26 +290,46 @@ class SlabDiffusion:
             ops.append(dist.P2POp(dist.irecv, self.halo_hi, self.rank + 1, g))
         return ops
 
-    def step(self, nsteps: int = 1) -> torch.Tensor:
+    def _step_nccl(self) -> None:
         nxl = self.f.shape[0]
-        for _ in range(nsteps):
-            ops = self._exchange_ops()
-            reqs = []
-            if ops:
-                if self.is_cuda:
-                    self.comm.wait_stream(torch.cuda.current_stream(self.f.device))
-                    with torch.cuda.stream(self.comm):
-                        reqs = dist.batch_isend_irecv(ops)
-                else:
+        ops = self._exchange_ops()
+        reqs = []
+        if ops:
+            if self.is_cuda:
+                self.comm.wait_stream(torch.cuda.current_stream(self.f.device))
+                with torch.cuda.stream(self.comm):
                     reqs = dist.batch_isend_irecv(ops)
-            # interior planes need no halo and overlap the exchange
-            if nxl > 2:
-                self.k.slab(self.f, self.fn, None, None, 1, nxl - 1)
-            for r in reqs:
-                r.wait()
-            self.k.slab(self.f, self.fn, self.halo_lo, self.halo_hi, 0, 1)
-            self.k.slab(self.f, self.fn, self.halo_lo, self.halo_hi, nxl - 1, nxl)
+            else:
+                reqs = dist.batch_isend_irecv(ops)
+        # interior planes need no halo and overlap the exchange
+        if nxl > 2:
+            self.k.slab(self.f, self.fn, None, None, 1, nxl - 1)
+        for r in reqs:
+            r.wait()
+        self.k.slab(self.f, self.fn, self.halo_lo, self.halo_hi, 0, 1)
+        self.k.slab(self.f, self.fn, self.halo_lo, self.halo_hi, nxl - 1, nxl)
+
+    def _step_p2p(self) -> None:
+        nxl = self.f.shape[0]
+        stream = torch.cuda.current_stream(self.f.device)
+        dist.barrier(group=self.ctrl)  # host-side: neighbours recorded their previous-step event
+        for _, _, _, ev in self._peer.values():
+            stream.wait_event(ev)
+        lo, hi = self._halo_ptrs()
+        if nxl > 2:
+            self.k.slab(self.f, self.fn, None, None, 1, nxl - 1)
+        self.k.slab(self.f, self.fn, lo, hi, 0, 1)
+        self.k.slab(self.f, self.fn, lo, hi, nxl - 1, nxl)
+        self.event.record(stream)
+
+    def step(self, nsteps: int = 1) -> torch.Tensor:
+        for _ in range(nsteps):
+            if self.transport == "p2p":
+                self._step_p2p()
+            else:
+                self._step_nccl()
             self.f, self.fn = self.fn, self.f
+            self.steps_done += 1
         return self.f
 
     def launches_per_step(self) -> int:
