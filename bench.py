@@ -52,8 +52,8 @@ def parse_args():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-diffusion", action="store_true")
     ap.add_argument("--no-configs", action="store_true", help="skip the BASELINE parity configs [0] and [1]")
-    ap.add_argument("--halo", choices=["p2p", "nccl"], default="p2p",
-                    help="diffusion halo transport for N>1: fused peer-memory reads (p2p) or NCCL send/recv")
+    ap.add_argument("--transport", choices=["p2p", "nccl"], default="p2p",
+                    help="N>1 data exchange: fused peer-memory (p2p: halo reads / position publish inside the kernels) or NCCL")
     ap.add_argument("--dist", action="store_true",
                     help="use the multi-GPU drivers (NCCL) even at world size 1 (smoke-tests the N>1 path)")
     ap.add_argument("--cpu-seconds", type=float, default=8.0, help="target CPU time per baseline sample")
@@ -309,24 +309,42 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         parallelism = "single GPU"
     else:
         plan_lo = rank * (n // world)
-        sim = ShardedLeapfrog(torch.from_numpy(pos_np[plan_lo:plan_lo + n // world]).to(dev),
-                              torch.from_numpy(vel_np[plan_lo:plan_lo + n // world]).to(dev), EPS, DT)
+        nb_transport = args.transport
+        try:
+            sim = ShardedLeapfrog(torch.from_numpy(pos_np[plan_lo:plan_lo + n // world]).to(dev),
+                                  torch.from_numpy(vel_np[plan_lo:plan_lo + n // world]).to(dev), EPS, DT,
+                                  transport=nb_transport)
+        except Exception as e:  # noqa: BLE001
+            print(f"p2p position transport unavailable ({e}); using NCCL", file=sys.stderr)
+            nb_transport = "nccl"
+            sim = ShardedLeapfrog(torch.from_numpy(pos_np[plan_lo:plan_lo + n // world]).to(dev),
+                                  torch.from_numpy(vel_np[plan_lo:plan_lo + n // world]).to(dev), EPS, DT,
+                                  transport=nb_transport)
         sim.step(1, close=False)
         n_local = n // world
+        steady = _lib.B2_KDK_REDUCE | _lib.B2_KDK_KICK_END | _lib.B2_KDK_KICK_DRIFT
 
         def step(evs):
+            hh = 0.5 * DT
             evs[0].record(stream)
-            sim.gather()
+            if nb_transport == "nccl":
+                sim.gather()
+            else:
+                sim._await_peers()
             evs[3].record(stream)
             sim.k.partials(sim.pos, sim.pos_all, sim.eps, sim.part)
             evs[1].record(stream)
-            hh = 0.5 * DT
-            sim.k.update(sim.pos, sim.vel, sim.acc, sim.part, sim.nch, hh, hh, DT,
-                         _lib.B2_KDK_REDUCE | _lib.B2_KDK_KICK_END | _lib.B2_KDK_KICK_DRIFT)
+            if nb_transport == "nccl":
+                sim.k.update(sim.pos, sim.vel, sim.acc, sim.part, sim.nch, hh, hh, DT, steady)
+            else:
+                sim._publish_update(sim.vel, sim.part, hh, hh, DT, steady)
             evs[2].record(stream)
 
         launches_per_step = 2
-        parallelism = f"i-shard x{world}, NCCL all_gather_into_tensor of positions per step"
+        parallelism = (f"i-shard x{world}, " + ("NCCL all_gather_into_tensor of positions per step"
+                                                  if nb_transport == "nccl" else
+                                                  "positions published to every peer by the update kernel "
+                                                  "(fused all-gather over peer memory)"))
 
     mk = lambda: [torch.cuda.Event(enable_timing=True) for _ in range(4)]  # noqa: E731
     for _ in range(args.warmup):
@@ -453,7 +471,7 @@ def run_diffusion(args, rank, world, dev, stream, peaks, barrier, max_over_ranks
         nxl = g // world
         gen = torch.Generator(device=dev).manual_seed(7 + rank)
         f_local = torch.rand((nxl, g, g), generator=gen, dtype=torch.float32, device=dev)
-        transport = args.halo
+        transport = args.transport
         try:
             sim = SlabDiffusion(f_local, *dargs, transport=transport)
         except Exception as e:  # noqa: BLE001 -- report and fall back to the NCCL transport

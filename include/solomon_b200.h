@@ -112,6 +112,14 @@ int b2_calc_acc_partials(int Ni, const float *ipos, int Nj, const float *jpos, f
 int b2_kdk_update(int n, float *pos, float *vel, float *acc, const float *partials, int nchunks,
                   float h_end, float h_begin, float dt, int phases, void *stream);
 
+/* Multi-GPU variant (fused all-gather): reads positions from pos_in, writes
+ * the updated (or, without B2_KDK_KICK_DRIFT, unchanged) positions to pos_out
+ * AND to each of the npeers (<= 8) peer buffers -- device addresses mapped
+ * with b2_ipc_import, i.e. other GPUs' position arrays over NVLink/NVSwitch. */
+int b2_kdk_update_publish(int n, const float *pos_in, float *pos_out, float *vel, float *acc,
+                          const float *partials, int nchunks, float h_end, float h_begin, float dt,
+                          int phases, float *const *peers, int npeers, void *stream);
+
 /* Whole single-device leapfrog: nsteps KDK steps of the self-gravitating
  * system pos[n] (acc must hold a(pos) on entry unless B2_INIT_ACC is set;
  * holds a(pos) on exit). Two kernel launches per step. */

@@ -42,6 +42,7 @@ SIGNATURES = {
     "b2_calc_acc": (_i, [_i, _p, _p, _i, _p, _f, _i, _p, _sz, _p]),
     "b2_calc_acc_partials": (_i, [_i, _p, _i, _p, _f, _i, _p, _p]),
     "b2_kdk_update": (_i, [_i, _p, _p, _p, _p, _i, _f, _f, _f, _i, _p]),
+    "b2_kdk_update_publish": (_i, [_i, _p, _p, _p, _p, _p, _i, _f, _f, _f, _i, _p, _i, _p]),
     "b2_leapfrog": (_i, [_i, _p, _p, _p, _f, _f, _i, _i, _p, _sz, _p]),
     "b2_leapfrog_workspace_bytes": (_sz, [_i, _i]),
     "b2_diffusion3d": (_i, [_i, _i, _i, _f, _f, _f, _f, _f, _p, _p, _p]),

@@ -302,11 +302,23 @@ __global__ void __launch_bounds__(128)
 }
 
 // ---------------------------------------------------------------------------
-// K2: fused reduce + kick(s) + drift. One particle per thread, float4 I/O.
+// K2: fused reduce + kick(s) + drift (+ publish). One particle per thread.
+//
+// Publish (multi-GPU fused all-gather): the new position is also
+// stored into every peer's position buffer (mapped over NVLink/NVSwitch via
+// CUDA IPC), so the all-gather of the next step's positions happens inside
+// the kernel that produces them -- no collective call.
+constexpr int kMaxPeers = 8;
+struct Peers {
+  float4* p[kMaxPeers];
+  int n;
+};
+constexpr int kPublish = 8;  // internal phase bit
+
 __global__ void __launch_bounds__(128)
-    k_kdk_update(int n, float4* __restrict__ pos, float4* __restrict__ vel, float4* __restrict__ acc,
-                 const float4* __restrict__ partials, int nchunks, float h_end, float h_begin, float dt,
-                 int phases) {
+    k_kdk_update(int n, const float4* pos_in, float4* pos_out, float4* __restrict__ vel, float4* __restrict__ acc,
+                 const float4* __restrict__ partials, int nchunks, float h_end, float h_begin, float dt, int phases,
+                 Peers peers) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   float4 a;
@@ -331,27 +343,36 @@ __global__ void __launch_bounds__(128)
       }
     }
     acc[i] = a;
-  } else {
+  } else if (phases & (B2_KDK_KICK_END | B2_KDK_KICK_DRIFT)) {
     a = acc[i];
   }
-  if (!(phases & (B2_KDK_KICK_END | B2_KDK_KICK_DRIFT))) return;
-  float4 v = vel[i];
-  if (phases & B2_KDK_KICK_END) {
-    v.x = __fmaf_rn(a.x, h_end, v.x);
-    v.y = __fmaf_rn(a.y, h_end, v.y);
-    v.z = __fmaf_rn(a.z, h_end, v.z);
+  const bool drift = phases & B2_KDK_KICK_DRIFT;
+  const bool publish = phases & kPublish;
+  float4 x;
+  if (drift || publish) x = pos_in[i];
+  if (phases & (B2_KDK_KICK_END | B2_KDK_KICK_DRIFT)) {
+    float4 v = vel[i];
+    if (phases & B2_KDK_KICK_END) {
+      v.x = __fmaf_rn(a.x, h_end, v.x);
+      v.y = __fmaf_rn(a.y, h_end, v.y);
+      v.z = __fmaf_rn(a.z, h_end, v.z);
+    }
+    if (drift) {
+      v.x = __fmaf_rn(a.x, h_begin, v.x);
+      v.y = __fmaf_rn(a.y, h_begin, v.y);
+      v.z = __fmaf_rn(a.z, h_begin, v.z);
+      x.x = __fmaf_rn(v.x, dt, x.x);
+      x.y = __fmaf_rn(v.y, dt, x.y);
+      x.z = __fmaf_rn(v.z, dt, x.z);
+    }
+    vel[i] = v;
   }
-  if (phases & B2_KDK_KICK_DRIFT) {
-    v.x = __fmaf_rn(a.x, h_begin, v.x);
-    v.y = __fmaf_rn(a.y, h_begin, v.y);
-    v.z = __fmaf_rn(a.z, h_begin, v.z);
-    float4 x = pos[i];
-    x.x = __fmaf_rn(v.x, dt, x.x);
-    x.y = __fmaf_rn(v.y, dt, x.y);
-    x.z = __fmaf_rn(v.z, dt, x.z);
-    pos[i] = x;
+  if (drift || publish) {
+    pos_out[i] = x;
+#pragma unroll
+    for (int k = 0; k < kMaxPeers; ++k)
+      if (k < peers.n) peers.p[k][i] = x;  // peer store over NVLink/NVSwitch
   }
-  vel[i] = v;
 }
 
 // ---------------------------------------------------------------------------
@@ -429,9 +450,15 @@ static int launch_partials(int Ni, const float4* ipos, int Nj, const float4* jpo
 }
 
 static int launch_update(int n, float4* pos, float4* vel, float4* acc, const float4* partials, int nchunks,
-                         float h_end, float h_begin, float dt, int phases, cudaStream_t s) {
+                         float h_end, float h_begin, float dt, int phases, cudaStream_t s,
+                         const float4* pos_in = nullptr, const Peers* peers = nullptr) {
   if (n <= 0) return B2_OK;
-  k_kdk_update<<<(n + 127) / 128, 128, 0, s>>>(n, pos, vel, acc, partials, nchunks, h_end, h_begin, dt, phases);
+  Peers pp{};
+  if (peers) pp = *peers;
+  if (!pos_in) pos_in = pos;
+  if (pp.n > 0 || pos_in != pos) phases |= kPublish;
+  k_kdk_update<<<(n + 127) / 128, 128, 0, s>>>(n, pos_in, pos, vel, acc, partials, nchunks, h_end, h_begin, dt, phases,
+                                               pp);
   return launch_status();
 }
 
@@ -508,6 +535,30 @@ int b2_kdk_update(int n, float* pos, float* vel, float* acc, const float* partia
   return launch_update(n, reinterpret_cast<float4*>(pos), reinterpret_cast<float4*>(vel),
                        reinterpret_cast<float4*>(acc), reinterpret_cast<const float4*>(partials), nchunks, h_end,
                        h_begin, dt, phases, as_stream(stream));
+}
+
+int b2_kdk_update_publish(int n, const float* pos_in, float* pos_out, float* vel, float* acc, const float* partials,
+                          int nchunks, float h_end, float h_begin, float dt, int phases, float* const* peers,
+                          int npeers, void* stream) {
+  int rc;
+  if (phases & ~(B2_KDK_REDUCE | B2_KDK_KICK_END | B2_KDK_KICK_DRIFT)) return B2_EINVAL;
+  if (npeers < 0 || npeers > kMaxPeers || (npeers > 0 && !peers)) return B2_EINVAL;
+  if ((rc = check_particles(n, acc)) || (rc = check_particles(n, pos_in)) || (rc = check_particles(n, pos_out)))
+    return rc;
+  if ((phases & B2_KDK_REDUCE) && ((rc = check_particles(n, partials)) || nchunks < 1)) return rc ? rc : B2_EINVAL;
+  if ((phases & (B2_KDK_KICK_END | B2_KDK_KICK_DRIFT)) && (rc = check_particles(n, vel))) return rc;
+  Peers pp{};
+  pp.n = npeers;
+  for (int k = 0; k < npeers; ++k) {
+    if ((rc = check_particles(n, peers[k]))) return rc;
+    pp.p[k] = reinterpret_cast<float4*>(peers[k]);
+  }
+  const int ph = phases | kPublish;
+  if (n <= 0) return B2_OK;
+  k_kdk_update<<<(n + 127) / 128, 128, 0, as_stream(stream)>>>(
+      n, reinterpret_cast<const float4*>(pos_in), reinterpret_cast<float4*>(pos_out), reinterpret_cast<float4*>(vel),
+      reinterpret_cast<float4*>(acc), reinterpret_cast<const float4*>(partials), nchunks, h_end, h_begin, dt, ph, pp);
+  return launch_status();
 }
 
 size_t b2_leapfrog_workspace_bytes(int n, int flags) {

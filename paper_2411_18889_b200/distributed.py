@@ -111,21 +111,38 @@ def shard_plan(n_total: int, group=None) -> ShardPlan:
 
 
 class ShardedLeapfrog:
-    """KDK leapfrog with i-particle shards and a position all-gather per step.
+    """KDK leapfrog with i-particle shards.
 
     ``pos_local``/``vel_local`` are this rank's block (rows [lo, hi) of the
-    global arrays). ``pos_all`` holds every rank's positions after a gather.
+    global arrays). ``pos_all`` holds every rank's positions.
+
+    ``transport="nccl"``: positions are all-gathered in place with NCCL before
+    every force evaluation.
+
+    ``transport="p2p"`` (fused all-gather): ``pos_all`` is double-buffered and
+    every rank maps every peer's two buffers (CUDA IPC). The update kernel that
+    drifts the positions stores them into all peers' next buffer as it writes
+    its own (``b2_kdk_update_publish``) -- the all-gather happens inside the
+    producing kernel. Before a force evaluation each rank's stream waits on all
+    peers' post-update interprocess events (a CPU-only gloo barrier makes sure
+    they were recorded). Double buffering removes the write-after-read hazard:
+    update k writes the buffer last read by force k-1, and every peer's force k
+    waits on all updates k-1, each of which followed that peer's force k-1.
     """
 
     def __init__(self, pos_local: torch.Tensor, vel_local: torch.Tensor, eps: float, dt: float, *, group=None,
-                 kernels=None, potential: bool = False, exact: bool = False):
+                 kernels=None, potential: bool = False, exact: bool = False, transport: str = "nccl"):
+        if transport not in ("nccl", "p2p"):
+            raise ValueError(f"unknown transport {transport!r}")
         self.group = group
+        self.transport = transport
         n_local = pos_local.shape[0]
         self.plan = shard_plan(n_local * dist.get_world_size(group), group)
         self.k = kernels or CudaNBodyKernels(potential, exact)
         dev = pos_local.device
-        self.pos_all = torch.empty((self.plan.n_total, 4), dtype=torch.float32, device=dev)
-        self.pos = self.pos_all[self.plan.lo:self.plan.hi]  # contiguous view: in-place gather source
+        nbuf = 2 if transport == "p2p" else 1
+        self._bufs = [torch.empty((self.plan.n_total, 4), dtype=torch.float32, device=dev) for _ in range(nbuf)]
+        self._cur = 0
         self.pos.copy_(pos_local)
         self.vel = vel_local.clone()
         self.acc = torch.empty_like(self.pos)
@@ -133,26 +150,140 @@ class ShardedLeapfrog:
         self.nch = self.k.nchunks(self.plan.n_total)
         self.part = torch.empty((max(self.nch, 1) * n_local, 4), dtype=torch.float32, device=dev)
         self._opened = False
+        if transport == "p2p":
+            self._setup_p2p()
         self.gather()
         self.k.partials(self.pos, self.pos_all, self.eps, self.part)
         self.k.update(None, None, self.acc, self.part, self.nch, 0.0, 0.0, 0.0, B2_KDK_REDUCE)
 
+    @property
+    def pos_all(self) -> torch.Tensor:
+        return self._bufs[self._cur]
+
+    @property
+    def pos(self) -> torch.Tensor:
+        return self._bufs[self._cur][self.plan.lo:self.plan.hi]  # contiguous view: in-place gather source
+
+    # ---- p2p transport -------------------------------------------------------
+    def _setup_p2p(self) -> None:
+        lib = _lib.load()
+        if not self.pos_all.is_cuda:
+            raise ValueError("transport='p2p' needs CUDA tensors")
+        self.ctrl = dist.new_group(backend="gloo") if dist.get_backend(self.group) != "gloo" else self.group
+        world, rank = self.plan.world, self.plan.rank
+        if world - 1 > 8:
+            raise ValueError("p2p transport supports up to 9 ranks (8 peers per kernel)")
+        hb = lib.b2_ipc_handle_bytes()
+        mine = []
+        for t in self._bufs:
+            h = ctypes.create_string_buffer(hb)
+            off = ctypes.c_size_t(0)
+            _lib.check(lib.b2_ipc_export(t.data_ptr(), h, ctypes.byref(off)), "ipc_export")
+            mine.append((h.raw, off.value))
+        self.event = torch.cuda.Event(enable_timing=False, interprocess=True)
+        self.event.record(torch.cuda.current_stream(self.pos_all.device))
+        everyone = [None] * world
+        dist.all_gather_object(everyone, {"bufs": mine, "event": bytes(self.event.ipc_handle())}, group=self.ctrl)
+        self._peers = []  # (ptrs per buffer, opened handles, event)
+        err = None
+        try:
+            for r in range(world):
+                if r == rank:
+                    continue
+                ptrs, opened = [], []
+                for h, off in everyone[r]["bufs"]:
+                    p = ctypes.c_void_p()
+                    _lib.check(lib.b2_ipc_import(ctypes.create_string_buffer(h, len(h)), off, ctypes.byref(p)),
+                               "ipc_import")
+                    ptrs.append(p.value)
+                    opened.append((p.value, off))
+                ev = torch.cuda.Event.from_ipc_handle(self.pos_all.device, everyone[r]["event"])
+                self._peers.append((ptrs, opened, ev))
+        except Exception as e:  # noqa: BLE001 -- agreed on below so that no rank is left in a collective
+            err = e
+        ok = torch.tensor([0 if err else 1], dtype=torch.int32)
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN, group=self.ctrl)
+        if not int(ok.item()):
+            self.close()
+            raise _lib.SolomonError(f"p2p position transport unavailable on some rank: {err or 'peer failure'}")
+
+    def _peer_ptrs(self, buf: int):
+        off = self.plan.lo * 16  # our slice inside each peer's buffer
+        arr = (ctypes.c_void_p * max(len(self._peers), 1))(*[p[0][buf] + off for p in self._peers])
+        return arr, len(self._peers)
+
+    def _publish_update(self, vel, partials, h_end, h_begin, dt, phases) -> None:
+        """Update + store the resulting positions into the next buffer here and on every peer."""
+        nxt = 1 - self._cur
+        peers, npeers = self._peer_ptrs(nxt)
+        dst = self._bufs[nxt][self.plan.lo:self.plan.hi]
+        ptr = lambda t: t.data_ptr() if t is not None else None  # noqa: E731
+        _lib.check(_lib.load().b2_kdk_update_publish(
+            self.acc.shape[0], self.pos.data_ptr(), dst.data_ptr(), ptr(vel), self.acc.data_ptr(), ptr(partials),
+            self.nch, float(h_end), float(h_begin), float(dt), phases, peers, npeers,
+            _lib.stream_handle(self.acc.device)), "kdk_update_publish")
+        self.event.record(torch.cuda.current_stream(self.acc.device))
+        self._cur = nxt
+
+    def _await_peers(self) -> None:
+        dist.barrier(group=self.ctrl)  # host-side: every peer recorded its latest post-update event
+        stream = torch.cuda.current_stream(self.pos_all.device)
+        for _, _, ev in self._peers:
+            stream.wait_event(ev)
+
+    def close(self) -> None:
+        if self.transport != "p2p" or not getattr(self, "_peers", None):
+            return
+        torch.cuda.synchronize(self.pos_all.device)
+        dist.barrier(group=self.ctrl)
+        lib = _lib.load()
+        for _, opened, _ in self._peers:
+            for p, off in opened:
+                lib.b2_ipc_close(p, off)
+        self._peers = []
+        dist.barrier(group=self.ctrl)
+
+    # ---- stepping --------------------------------------------------------------
     def gather(self) -> None:
-        _all_gather_inplace(self.pos_all, self.pos, self.group)
+        """Make pos_all hold every rank's current positions."""
+        if self.transport == "nccl":
+            _all_gather_inplace(self.pos_all, self.pos, self.group)
+            return
+        # publish our slice of the current buffer into every peer's current buffer
+        peers, npeers = self._peer_ptrs(self._cur)
+        _lib.check(_lib.load().b2_kdk_update_publish(
+            self.pos.shape[0], self.pos.data_ptr(), self.pos.data_ptr(), None, self.pos.data_ptr(), None, 1,
+            0.0, 0.0, 0.0, 0, peers, npeers, _lib.stream_handle(self.pos.device)), "publish")
+        self.event.record(torch.cuda.current_stream(self.pos.device))
+        self._await_peers()
 
     def step(self, nsteps: int = 1, *, close: bool = True) -> None:
         """Advance ``nsteps``; with ``close`` the velocities are synchronised (closing half-kick applied)."""
         h = 0.5 * self.dt
         for s in range(nsteps):
-            if not self._opened:
-                self.k.update(self.pos, self.vel, self.acc, None, self.nch, 0.0, h, self.dt, B2_KDK_KICK_DRIFT)
-                self._opened = True
-            self.gather()
-            self.k.partials(self.pos, self.pos_all, self.eps, self.part)
-            last = close and s + 1 == nsteps
-            phases = B2_KDK_REDUCE | B2_KDK_KICK_END | (0 if last else B2_KDK_KICK_DRIFT)
-            self.k.update(self.pos, self.vel, self.acc, self.part, self.nch, h, h, self.dt, phases)
-            self._opened = not last
+            if self.transport == "nccl":
+                if not self._opened:
+                    self.k.update(self.pos, self.vel, self.acc, None, self.nch, 0.0, h, self.dt, B2_KDK_KICK_DRIFT)
+                    self._opened = True
+                self.gather()
+                self.k.partials(self.pos, self.pos_all, self.eps, self.part)
+                last = close and s + 1 == nsteps
+                phases = B2_KDK_REDUCE | B2_KDK_KICK_END | (0 if last else B2_KDK_KICK_DRIFT)
+                self.k.update(self.pos, self.vel, self.acc, self.part, self.nch, h, h, self.dt, phases)
+                self._opened = not last
+            else:
+                if not self._opened:
+                    # WAR: the buffer this update publishes into was read by the peers'
+                    # last force evaluation -- wait for their last update (which followed it).
+                    self._await_peers()
+                    self._publish_update(self.vel, None, 0.0, h, self.dt, B2_KDK_KICK_DRIFT)
+                    self._opened = True
+                self._await_peers()
+                self.k.partials(self.pos, self.pos_all, self.eps, self.part)
+                last = close and s + 1 == nsteps
+                phases = B2_KDK_REDUCE | B2_KDK_KICK_END | (0 if last else B2_KDK_KICK_DRIFT)
+                self._publish_update(self.vel, self.part, h, h, self.dt, phases)
+                self._opened = not last
 
     def launches_per_step(self) -> int:
         return 2
