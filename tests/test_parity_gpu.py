@@ -358,18 +358,33 @@ def test_stream_ordering_on_side_stream(b2, restatement):
     assert bits_equal(fn.cpu().numpy(), restatement.diffusion3d(f0, 0.1, 0.1, 0.1, 1e-3, 1.0))
 
 
+def _fp64_acc(ipos, jpos, eps: float) -> np.ndarray:
+    """Ground truth in FP64 on the GPU (test-only)."""
+    ip, jp = ipos.double(), jpos.double()
+    out = []
+    for blk in ip.split(32):
+        r = jp[None, :, :3] - blk[:, None, :3]
+        r2 = (r * r).sum(-1) + eps * eps
+        w = jp[None, :, 3] / (r2 * r2.sqrt())
+        out.append((r * w[..., None]).sum(1))
+    return torch.cat(out).cpu().numpy()
+
+
 def test_large_n_int_indexing(b2):
-    """N = 2^22 single-GPU force (the configs[3] total): finite, momentum-balanced (sampled)."""
+    """N = 2^22 (the configs[3] total) on one GPU: sampled i against all j. Against FP64 truth the
+    chunked fast path is at least as accurate as the reference's sequential FP32 sum."""
+    import oracle
+
     n = 1 << 22
     pos, _ = b2.plummer_numpy(n, 42)
     p = dev(pos)
-    sub = p[: 1 << 12].contiguous()
-    acc = b2.accelerations(sub, 2.0 ** -6, p).cpu().numpy()
+    sub = p[:256].contiguous()
+    acc = b2.accelerations(sub, 2.0 ** -6, p).cpu().numpy()[:, :3]
     assert np.all(np.isfinite(acc))
-    import oracle
-
-    want = oracle.Restatement().calc_acc(pos[:256], pos, 2.0 ** -6)
-    assert rel_l2(acc[:256], want) <= 1e-4
+    truth = _fp64_acc(sub, p, 2.0 ** -6)
+    ref = oracle.Restatement().calc_acc(pos[:256], pos, 2.0 ** -6)[:, :3]
+    err_ours, err_ref = rel_l2(acc, truth), rel_l2(ref, truth)
+    assert err_ours <= max(1.5 * err_ref, 1e-5) and err_ours < 1e-4, (err_ours, err_ref)
 
 
 @pytest.mark.parametrize("shape", [(64, 48, 40), (100, 33, 64), (17, 8, 12)])
