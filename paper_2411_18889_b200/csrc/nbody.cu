@@ -266,6 +266,7 @@ __global__ void __launch_bounds__(BLOCK, MINB)
   }
 }
 
+
 // ---------------------------------------------------------------------------
 // K1 exact: the reference's arithmetic, bit for bit (IEEE sqrt and divide,
 // explicit roundings so nvcc cannot contract, sequential j). One i per thread.

@@ -84,6 +84,12 @@ __global__ void __launch_bounds__(256) k_pattern(float* out, int iters, const fl
         if (MODE == 1) acc[c] = __ffma2_rn(x[c], y[0], acc[c]);
         if (MODE == 2) sacc[c] = fmaf(sx[c], sy[c], sacc[c]);
         if (MODE == 3) acc[c] = __ffma2_rn(x[c], x[c], acc[c]);
+        if (MODE == 4) acc[c] = __fadd2_rn(acc[c], x[c]);
+        if (MODE == 5) acc[c] = __fmul2_rn(acc[c], x[c]);
+        if (MODE == 6) acc[c] = __ffma2_rn(acc[c], make_float2(s0, s0), x[c]);
+        if (MODE == 7) acc[c] = __fadd2_rn(acc[c], make_float2(s0, s0));
+        if (MODE == 8) acc[c] = __fmul2_rn(acc[c], make_float2(s0, s0));
+        if (MODE == 9) acc[c] = __ffma2_rn(acc[c], make_float2(s0, s0), make_float2(s0, s0));
       }
   }
   float s = 0.f;
@@ -106,7 +112,13 @@ extern "C" double solomon_probe_pattern_tflops(int mode) {
       case 0: k_pattern<0><<<blocks, threads>>>(d, iters, seed); break;
       case 1: k_pattern<1><<<blocks, threads>>>(d, iters, seed); break;
       case 2: k_pattern<2><<<blocks, threads>>>(d, iters, seed); break;
-      default: k_pattern<3><<<blocks, threads>>>(d, iters, seed); break;
+      case 3: k_pattern<3><<<blocks, threads>>>(d, iters, seed); break;
+      case 4: k_pattern<4><<<blocks, threads>>>(d, iters, seed); break;
+      case 5: k_pattern<5><<<blocks, threads>>>(d, iters, seed); break;
+      case 6: k_pattern<6><<<blocks, threads>>>(d, iters, seed); break;
+      case 7: k_pattern<7><<<blocks, threads>>>(d, iters, seed); break;
+      case 8: k_pattern<8><<<blocks, threads>>>(d, iters, seed); break;
+      default: k_pattern<9><<<blocks, threads>>>(d, iters, seed); break;
     }
   };
   launch();
@@ -127,7 +139,8 @@ extern "C" double solomon_probe_pattern_tflops(int mode) {
   cudaFree(d);
   cudaFree(seed);
   const double lanes = (mode == 2) ? 1.0 : 2.0;
-  return double(threads) * blocks * iters * 8 * 8 * lanes * 2 / (best * 1e-3) / 1e12;
+  const double flop = (mode == 4 || mode == 5 || mode == 7 || mode == 8) ? 1.0 : 2.0;  // add/mul count 1
+  return double(threads) * blocks * iters * 8 * 8 * lanes * flop / (best * 1e-3) / 1e12;
 }
 
 // n-body inner-loop probes: j-particles from __constant__ (uniform datapath)
