@@ -569,6 +569,10 @@ def run_parity_configs(dev):
     cpu_ms = (time.perf_counter() - t0) * 1e3
     gp, gv = lf.pos.cpu().numpy(), lf.vel.cpu().numpy()
     rel = lambda a, b: float(np.linalg.norm(a - b) / np.linalg.norm(b))  # noqa: E731
+    # physics check (the integrator has no reference): total energy drift over the 16 steps
+    p0 = torch.from_numpy(pos).to(dev)
+    e_start = sum(b2.energy(p0, torch.from_numpy(vel).to(dev), b2.accelerations(p0, eps, potential=True), eps))
+    e_end = sum(b2.energy(lf.pos, lf.vel, b2.accelerations(lf.pos, eps, potential=True), eps))
     out["nbody_4096_plummer_kdk16"] = {
         "config": "BASELINE configs[0]: N=4096 Plummer FP32, 16 leapfrog steps",
         "gpu_ms": gpu_ms, "gpu_launches": 2 * steps + 1,
@@ -578,6 +582,7 @@ def run_parity_configs(dev):
         "cpu_cores": int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1)),
         "parity_relL2": {"pos": rel(gp[:, :3], wp[:, :3]), "vel": rel(gv[:, :3], wv[:, :3])},
         "tolerance": {"pos": 1e-5, "vel": 1e-4},
+        "energy": {"start": e_start, "end": e_end, "rel_drift": abs(e_end - e_start) / abs(e_start)},
     }
     # configs[1]: 128^3 diffusion, 100 steps
     g, dsteps = 128, 100
