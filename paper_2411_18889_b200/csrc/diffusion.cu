@@ -643,10 +643,12 @@ static bool plan_march2(int nx, int ny, int nz, March2Plan& mp) {
 
 template <int S1, int S2>
 static void launch_march2_t(const March2Plan& mp, const March2Args& a, cudaStream_t s) {
-  static bool set = false;
-  if (!set) {
+  static bool set[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (!set[dev]) {  // per device: the opt-in is a per-context function attribute
     cudaFuncSetAttribute(k_diffusion_march2<S1, S2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    set = true;
+    set[dev] = true;
   }
   k_diffusion_march2<S1, S2><<<mp.grid, kMarchThreads, mp.smem, s>>>(a);
 }
@@ -683,10 +685,12 @@ static int launch_step(int nx, int ny, int nz, const Coefs& c, const float* f, c
     switch (mp.S) {
 #define B2_MARCH_CASE(SV)                                                                                     \
   case SV: {                                                                                                  \
-    static bool attr_set = false;                                                                             \
-    if (!attr_set) {                                                                                          \
+    static bool attr_set[64] = {};                                                                            \
+    int dev_ = 0;                                                                                             \
+    cudaGetDevice(&dev_);                                                                                     \
+    if (!attr_set[dev_]) {                                                                                    \
       cudaFuncSetAttribute(k_diffusion_march<SV>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024); \
-      attr_set = true;                                                                                        \
+      attr_set[dev_] = true;                                                                                  \
     }                                                                                                         \
     k_diffusion_march<SV><<<mp.grid, kMarchThreads, mp.smem, s>>>(a);                                         \
     break;                                                                                                    \
