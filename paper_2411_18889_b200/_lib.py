@@ -65,6 +65,8 @@ class SolomonError(RuntimeError):
 def load(path: pathlib.Path | str | None = None) -> ctypes.CDLL:
     """Load (once) and type the C-ABI library. Raises if it is missing."""
     global _lib
+    if _lib is not None and path is None:  # fast path: no lock once loaded
+        return _lib
     with _lock:
         if _lib is not None and path is None:
             return _lib
