@@ -11,12 +11,14 @@
 //       a += r*w  (3 FMA); [pot: a.w = fma(r2, w, a.w)]           (:18-23)
 //
 // Fast kernel design: FP32 CUDA-core work (not a contraction,
-// so no tensor cores). Each thread owns IPT=8 i-particles as 4 packed pairs
-// and evaluates every interaction with Blackwell's packed FP32 instructions
-// (FADD2/FFMA2/FMUL2 -- 6 issue slots per 2 interactions instead of 12) plus
-// MUFU.RSQ. j-particles stream through shared memory in BLOCK-sized tiles,
-// double-buffered, pre-duplicated as {x,x,y,y},{z,z,m,m} so one LDS.128 feeds
-// a packed operand pair with no MOVs. Nj is cut into fixed chunks whose size
+// so no tensor cores). Each thread owns IPT=16 i-particles as 8 packed pairs
+// (default variant 0: 128 threads, 2 CTAs/SM) and evaluates every interaction
+// with Blackwell's packed FP32 instructions (FADD2/FFMA2/FMUL2 -- 6 issue
+// slots per 2 interactions instead of 12) plus MUFU.RSQ. j-particles stream
+// through shared memory in BLOCK-sized tiles, double-buffered; one LDS.128 per
+// j feeds the packed ops as scalar-broadcast operands (SCHED 2; the older
+// pre-duplicated {x,x,y,y},{z,z,m,m} layout survives as SCHED 0/1 variants).
+// Nj is cut into fixed chunks whose size
 // depends on Nj only; each (i-tile, j-chunk) is one CTA of work, giving >50
 // waves at N=2^20 (no tail), and per-chunk partial sums are combined in a
 // fixed order by the K2 update kernel (deterministic, shard-invariant).
