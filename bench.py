@@ -575,7 +575,10 @@ def run_parity_configs(dev):
     e_end = sum(b2.energy(lf.pos, lf.vel, b2.accelerations(lf.pos, eps, potential=True), eps))
     out["nbody_4096_plummer_kdk16"] = {
         "config": "BASELINE configs[0]: N=4096 Plummer FP32, 16 leapfrog steps",
-        "gpu_ms": gpu_ms, "gpu_launches": 2 * steps + 1,
+        "gpu_ms": gpu_ms, "gpu_launches": 1,
+        "path": "b2_leapfrog -> k_leapfrog_small (all 16 KDK steps in one persistent launch, positions "
+                "exchanged between CTAs as tagged 16-byte words; + one memset), bit-identical to the "
+                "two-kernel-per-step path",
         "gpu_ginteractions_per_s": n * n * steps / (gpu_ms * 1e-3) / 1e9,
         "cpu_ms": cpu_ms, "cpu_kind": "port (oracle/solomon_oracle.c KDK around the restated calc_acc; "
                                       "the reference has no integrator)",

@@ -122,7 +122,9 @@ int b2_kdk_update_publish(int n, const float *pos_in, float *pos_out, float *vel
 
 /* Whole single-device leapfrog: nsteps KDK steps of the self-gravitating
  * system pos[n] (acc must hold a(pos) on entry unless B2_INIT_ACC is set;
- * holds a(pos) on exit). Two kernel launches per step. */
+ * holds a(pos) on exit). Small systems (n <= 32 x SMs, fast arithmetic) run
+ * every step in one persistent launch; otherwise two launches per step. Both
+ * give the same bits. */
 #define B2_INIT_ACC 4
 int b2_leapfrog(int n, float *pos, float *vel, float *acc, float eps, float dt, int nsteps, int flags,
                 void *workspace, size_t workspace_bytes, void *stream);

@@ -450,3 +450,37 @@ def test_diffusion_run_fallback_paths_bit_identical():
         env = dict(os.environ, **extra)
         out = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True)
         assert out.returncode == 0 and "ok" in out.stdout, (extra, out.stderr[-2000:])
+
+
+def test_leapfrog_persistent_small_n_bit_identical(tmp_path):
+    """The one-launch small-N leapfrog (k_leapfrog_small: tagged-position exchange between
+    persistent CTAs) == the two-kernel path (partials + fused update), bit for bit, across N,
+    step counts, the potential and the B2_INIT_ACC opening."""
+    import os
+    import subprocess
+    import sys
+
+    code = (
+        "import sys, numpy as np, torch; sys.path.insert(0, '.')\n"
+        "import paper_2411_18889_b200 as b2\n"
+        "out = {}\n"
+        "for n, steps, pot in [(4096, 16, False), (4096, 3, True), (3000, 5, False), (100, 4, True),\n"
+        "                      (4736, 2, False), (130, 0, False), (2048, 1, False)]:\n"
+        "    pos, vel = b2.plummer_numpy(n, 7)\n"
+        "    lf = b2.Leapfrog(torch.from_numpy(pos).cuda(), torch.from_numpy(vel).cuda(), 2.0 ** -6, 2.0 ** -7,\n"
+        "                     potential=pot)\n"
+        "    lf.step(steps)\n"
+        "    lf.step(1)\n"
+        "    for k, t in (('p', lf.pos), ('v', lf.vel), ('a', lf.acc)):\n"
+        "        out[f'{n}_{steps}_{pot}_{k}'] = t.cpu().numpy()\n"
+        "np.savez(sys.argv[1], **out)\n")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    res = {}
+    for flag in ("1", "0"):
+        dst = tmp_path / f"lf{flag}.npz"
+        env = dict(os.environ, SOLOMON_NBODY_PERSISTENT=flag)
+        r = subprocess.run([sys.executable, "-c", code, str(dst)], cwd=root, env=env, capture_output=True, text=True)
+        assert r.returncode == 0, r.stderr[-2000:]
+        res[flag] = np.load(dst)
+    for k in res["0"].files:
+        assert bits_equal(res["1"][k], res["0"][k]), k
