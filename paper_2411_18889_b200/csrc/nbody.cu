@@ -13,8 +13,8 @@
 // Fast kernel design: FP32 CUDA-core work (not a contraction,
 // so no tensor cores). Each thread owns IPT=16 i-particles as 8 packed pairs
 // (default variant 0: 128 threads, 2 CTAs/SM) and evaluates every interaction
-// with Blackwell's packed FP32 instructions (FADD2/FFMA2/FMUL2 -- 6 issue
-// slots per 2 interactions instead of 12) plus MUFU.RSQ. j-particles stream
+// with Blackwell's packed FP32 instructions (FADD2/FFMA2/FMUL2 -- 12 issue
+// slots per 2 interactions instead of 24) plus MUFU.RSQ. j-particles stream
 // through shared memory in BLOCK-sized tiles, double-buffered; one LDS.128 per
 // j feeds the packed ops as scalar-broadcast operands (SCHED 2; the older
 // pre-duplicated {x,x,y,y},{z,z,m,m} layout survives as SCHED 0/1 variants).
