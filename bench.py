@@ -46,7 +46,8 @@ def parse_args():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--n", type=int, default=None, help="override particle count")
+    ap.add_argument("--particles", "--n", dest="n", type=int, default=None,
+                    help="override particle count (use --particles under torchrun: --n clashes with its options)")
     ap.add_argument("--grid", type=int, default=None, help="override diffusion grid edge")
     ap.add_argument("--dsteps", type=int, default=50, help="timed diffusion steps")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -637,13 +638,9 @@ def main():
             print(json.dumps(out), flush=True)
         return
     if world > 1 or args.dist:
-        import torch
-        import torch.distributed as dist
+        from paper_2411_18889_b200.distributed import init_distributed
 
-        torch.cuda.set_device(local_rank)
-        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        os.environ.setdefault("MASTER_PORT", "29511")
-        dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", local_rank))
+        init_distributed("nccl", timeout_s=900.0)  # a lost rank fails the run instead of hanging it
     out = run_ours(args, rank, world, local_rank)
     if rank == 0:
         print(json.dumps(out), flush=True)

@@ -14,6 +14,7 @@ uniform particle setup, grid setup, and the multi-GPU partitioning in
 (include/solomon_b200.h); there is no CPU fallback.
 """
 from ._lib import SolomonError, load  # noqa: F401
+from .checkpoint import load as load_checkpoint, save as save_checkpoint  # noqa: F401
 from .diffusion import Diffusion3D, coefficients, diffusion3d, diffusion3d_slab, init_grid  # noqa: F401
 from .nbody import (  # noqa: F401
     Leapfrog,

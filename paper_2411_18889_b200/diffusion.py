@@ -97,6 +97,7 @@ class Diffusion3D:
             raise ValueError("f must be [nx, ny, nz]")
         _grid(self.f, self.f.numel(), "f")
         self._fn = torch.empty_like(self.f)
+        self.steps = 0
 
     @property
     def field(self) -> torch.Tensor:
@@ -112,7 +113,29 @@ class Diffusion3D:
                                             stream_handle(self.f.device)), "diffusion3d_run")
         if in_fn.value:
             self.f, self._fn = self._fn, self.f
+        self.steps += int(nsteps)
         return self.f
+
+    # ---- checkpoint / resume -----------------------------------
+    def state_dict(self) -> dict:
+        return {"kind": "Diffusion3D", "f": self.f.clone(), "dx": self.dx, "dy": self.dy, "dz": self.dz,
+                "dt": self.dt, "kappa": self.kappa, "steps": self.steps}
+
+    def load_state_dict(self, sd: dict) -> None:
+        if sd.get("kind") != "Diffusion3D":
+            raise ValueError(f"not a Diffusion3D checkpoint: {sd.get('kind')!r}")
+        if tuple(sd["f"].shape) != tuple(self.f.shape):
+            raise ValueError(f"checkpoint grid {tuple(sd['f'].shape)} != {tuple(self.f.shape)}")
+        if (sd["dx"], sd["dy"], sd["dz"], sd["dt"], sd["kappa"]) != (self.dx, self.dy, self.dz, self.dt, self.kappa):
+            raise ValueError("checkpoint coefficients differ from this run's")
+        self.f.copy_(sd["f"])
+        self.steps = int(sd["steps"])
+
+    @classmethod
+    def from_state_dict(cls, sd: dict, device: torch.device | str = "cuda") -> "Diffusion3D":
+        sim = cls(sd["f"].to(device).clone(), sd["dx"], sd["dy"], sd["dz"], sd["dt"], sd["kappa"])
+        sim.steps = int(sd["steps"])
+        return sim
 
 
 def init_grid(nx: int, ny: int, nz: int, kind: str = "uniform", seed: int = 7,

@@ -24,6 +24,8 @@ fails loudly without it.
 from __future__ import annotations
 
 import ctypes
+import datetime
+import os
 from dataclasses import dataclass
 
 import torch
@@ -79,6 +81,28 @@ def _all_gather_inplace(out: torch.Tensor, local: torch.Tensor, group=None) -> N
     world = dist.get_world_size(group)
     parts = list(out.chunk(world))
     dist.all_gather(parts, local.clone(), group=group)
+
+
+def init_distributed(backend: str = "nccl", timeout_s: float = 600.0) -> tuple[int, int, int]:
+    """One process per GPU (torchrun env: RANK, WORLD_SIZE, LOCAL_RANK, MASTER_*).
+
+    Binds the process to its GPU, defaults the rendezvous to 127.0.0.1, and sets a
+    collective timeout so a lost peer fails the job instead of hanging it (SURVEY.md
+    §5: failure detection = NCCL timeouts; nothing elastic). Returns (rank, world,
+    local_rank).
+    """
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", "29511")
+    kw = {}
+    if backend == "nccl":
+        torch.cuda.set_device(local)
+        kw["device_id"] = torch.device("cuda", local)
+    dist.init_process_group(backend, rank=rank, world_size=world, timeout=datetime.timedelta(seconds=timeout_s),
+                            **kw)
+    return rank, world, local
 
 
 # ---------------------------------------------------------------------------
@@ -150,6 +174,7 @@ class ShardedLeapfrog:
         self.nch = self.k.nchunks(self.plan.n_total)
         self.part = torch.empty((max(self.nch, 1) * n_local, 4), dtype=torch.float32, device=dev)
         self._opened = False
+        self.steps = 0
         if transport == "p2p":
             self._setup_p2p()
         self.gather()
@@ -284,9 +309,35 @@ class ShardedLeapfrog:
                 phases = B2_KDK_REDUCE | B2_KDK_KICK_END | (0 if last else B2_KDK_KICK_DRIFT)
                 self._publish_update(self.vel, self.part, h, h, self.dt, phases)
                 self._opened = not last
+            self.steps += 1
 
     def launches_per_step(self) -> int:
         return 2
+
+    # ---- checkpoint / resume -----------------------------------
+    def state_dict(self) -> dict:
+        """This rank's shard. ``opened`` records a pending opening half-kick
+        (``step(close=False)``), so a resumed run continues bit for bit."""
+        return {"kind": "ShardedLeapfrog", "n_total": self.plan.n_total, "world": self.plan.world,
+                "rank": self.plan.rank, "pos": self.pos.clone(), "vel": self.vel.clone(), "acc": self.acc.clone(),
+                "eps": self.eps, "dt": self.dt, "opened": self._opened, "steps": self.steps}
+
+    def load_state_dict(self, sd: dict) -> None:
+        """Collective: every rank loads its own shard, then positions are re-gathered."""
+        if sd.get("kind") != "ShardedLeapfrog":
+            raise ValueError(f"not a ShardedLeapfrog checkpoint: {sd.get('kind')!r}")
+        want = (self.plan.n_total, self.plan.world, self.plan.rank)
+        if (sd["n_total"], sd["world"], sd["rank"]) != want:
+            raise ValueError(f"checkpoint is for (N, world, rank) = {(sd['n_total'], sd['world'], sd['rank'])}, "
+                             f"this run is {want}")
+        if (sd["eps"], sd["dt"]) != (self.eps, self.dt):
+            raise ValueError("checkpoint eps/dt differ from this run's")
+        self.pos.copy_(sd["pos"])
+        self.vel.copy_(sd["vel"])
+        self.acc.copy_(sd["acc"])
+        self._opened = bool(sd["opened"])
+        self.steps = int(sd["steps"])
+        self.gather()
 
 
 # ---------------------------------------------------------------------------
@@ -324,6 +375,7 @@ class SlabDiffusion:
         self.k = kernels or CudaSlabKernels(dx, dy, dz, dt, kappa)
         self.f = f_local.contiguous().clone()
         self.fn = torch.empty_like(self.f)
+        self._bufs = (self.f, self.fn)  # state s lives in _bufs[s % 2]
         ny, nz = self.f.shape[1:]
         self.has_lo = self.rank > 0
         self.has_hi = self.rank < self.world - 1
@@ -465,3 +517,25 @@ class SlabDiffusion:
 
     def launches_per_step(self) -> int:
         return 3 if self.f.shape[0] > 2 else 2
+
+    # ---- checkpoint / resume -----------------------------------
+    def state_dict(self) -> dict:
+        return {"kind": "SlabDiffusion", "world": self.world, "rank": self.rank, "f": self.f.clone(),
+                "steps": self.steps_done}
+
+    def load_state_dict(self, sd: dict) -> None:
+        """Collective: every rank loads its own slab. The field goes into the buffer
+        that holds state ``steps`` (the p2p transport addresses peers by that parity)."""
+        if sd.get("kind") != "SlabDiffusion":
+            raise ValueError(f"not a SlabDiffusion checkpoint: {sd.get('kind')!r}")
+        if (sd["world"], sd["rank"]) != (self.world, self.rank) or tuple(sd["f"].shape) != tuple(self.f.shape):
+            raise ValueError("checkpoint is for a different decomposition")
+        s = int(sd["steps"])
+        self.f, self.fn = self._bufs[s % 2], self._bufs[1 - s % 2]
+        self.f.copy_(sd["f"])
+        self.steps_done = s
+        if self.transport == "p2p":
+            self.event.record(torch.cuda.current_stream(self.f.device))  # neighbours wait for the copy
+        elif self.is_cuda:
+            torch.cuda.current_stream(self.f.device).synchronize()
+        dist.barrier(group=self.group)

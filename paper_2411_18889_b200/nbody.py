@@ -113,6 +113,7 @@ class Leapfrog:
         self._flags = _flags(self.potential, self.exact)
         self._ws = torch.empty(max(int(load().b2_leapfrog_workspace_bytes(n, self._flags)), 16),
                                dtype=torch.uint8, device=self.pos.device)
+        self.steps = 0
         self._run(0, init=True)
 
     def _run(self, nsteps: int, init: bool = False) -> None:
@@ -125,9 +126,36 @@ class Leapfrog:
 
     def step(self, nsteps: int = 1) -> None:
         self._run(nsteps)
+        self.steps += nsteps
 
     def kernel_launches_per_step(self) -> int:
         return 2
+
+    # ---- checkpoint / resume -----------------------------------
+    def state_dict(self) -> dict:
+        """Positions, velocities (synchronised: every step closes with its half-kick),
+        accelerations a(pos) and the step count -- everything a resumed run needs."""
+        return {"kind": "Leapfrog", "pos": self.pos.clone(), "vel": self.vel.clone(), "acc": self.acc.clone(),
+                "eps": self.eps, "dt": self.dt, "potential": self.potential, "exact": self.exact,
+                "steps": self.steps}
+
+    def load_state_dict(self, sd: dict) -> None:
+        if sd.get("kind") != "Leapfrog":
+            raise ValueError(f"not a Leapfrog checkpoint: {sd.get('kind')!r}")
+        if tuple(sd["pos"].shape) != tuple(self.pos.shape):
+            raise ValueError(f"checkpoint holds {tuple(sd['pos'].shape)} particles, this run {tuple(self.pos.shape)}")
+        if (sd["eps"], sd["dt"], sd["potential"], sd["exact"]) != (self.eps, self.dt, self.potential, self.exact):
+            raise ValueError("checkpoint eps/dt/potential/exact differ from this run's")
+        self.pos.copy_(sd["pos"])
+        self.vel.copy_(sd["vel"])
+        self.acc.copy_(sd["acc"])
+        self.steps = int(sd["steps"])
+
+    @classmethod
+    def from_state_dict(cls, sd: dict, device: torch.device | str = "cuda") -> "Leapfrog":
+        lf = cls(sd["pos"].to(device), sd["vel"].to(device), sd["eps"], sd["dt"], sd["potential"], sd["exact"])
+        lf.load_state_dict(sd)
+        return lf
 
 
 def leapfrog_kdk(pos: torch.Tensor, vel: torch.Tensor, eps: float, dt: float, nsteps: int, *,

@@ -156,3 +156,91 @@ def test_shard_plan_requires_divisible_n():
 
     p = ShardPlan(1 << 22, 8, 3)
     assert (p.n_local, p.lo, p.hi) == (1 << 19, 3 << 19, 4 << 19)
+
+
+def _ckpt_nbody_worker(rank, world, port, n, ckpt, out_path):
+    """4 steps straight vs 2 (left open: pending half-kick) + checkpoint + fresh driver + resume + 2."""
+    _init(rank, world, port)
+    from paper_2411_18889_b200 import checkpoint
+    from paper_2411_18889_b200.distributed import ShardedLeapfrog
+    from paper_2411_18889_b200.nbody import plummer_numpy
+
+    pos, vel = plummer_numpy(n, 5)
+    nl = n // world
+    mk = lambda: ShardedLeapfrog(torch.from_numpy(pos[rank * nl:(rank + 1) * nl]),  # noqa: E731
+                                 torch.from_numpy(vel[rank * nl:(rank + 1) * nl]), 2.0 ** -6, 2.0 ** -7,
+                                 kernels=OracleNBodyKernels(64))
+    a = mk()
+    a.step(4)
+    b = mk()
+    b.step(2, close=False)
+    checkpoint.save(b, ckpt)
+    c = mk()
+    checkpoint.load(c, ckpt)
+    c.step(2)
+    ok = all(np.array_equal(x.numpy().view(np.uint32), y.numpy().view(np.uint32))
+             for x, y in ((a.pos, c.pos), (a.vel, c.vel), (a.acc, c.acc))) and c.steps == 4
+    flags = [None] * world
+    dist.all_gather_object(flags, ok)
+    if rank == 0:
+        np.save(out_path, np.array(flags))
+    dist.destroy_process_group()
+
+
+def _ckpt_diff_worker(rank, world, port, shape, ckpt, out_path):
+    _init(rank, world, port)
+    from paper_2411_18889_b200 import checkpoint
+    from paper_2411_18889_b200.distributed import SlabDiffusion
+
+    f0 = np.random.default_rng(8).random(shape, dtype=np.float32)
+    args = (0.1, 0.12, 0.09, 1e-3, 1.0)
+    nl = shape[0] // world
+    mk = lambda: SlabDiffusion(torch.from_numpy(f0[rank * nl:(rank + 1) * nl].copy()), *args,  # noqa: E731
+                               kernels=OracleSlabKernels(*args))
+    a = mk()
+    a.step(5)
+    b = mk()
+    b.step(3)
+    checkpoint.save(b, ckpt)
+    c = mk()
+    checkpoint.load(c, ckpt)
+    c.step(2)
+    ok = np.array_equal(a.f.numpy().view(np.uint32), c.f.numpy().view(np.uint32)) and c.steps_done == 5
+    flags = [None] * world
+    dist.all_gather_object(flags, ok)
+    if rank == 0:
+        np.save(out_path, np.array(flags))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [1, 2])
+def test_sharded_leapfrog_checkpoint_resume_bit_identical(tmp_path, world):
+    out = tmp_path / "ok.npy"
+    mp.spawn(_ckpt_nbody_worker, args=(world, _free_port(), 256, str(tmp_path / "nb.{rank}.pt"), str(out)),
+             nprocs=world, join=True)
+    assert np.load(out).all()
+    assert sorted(p.name for p in tmp_path.glob("nb.*.pt")) == [f"nb.{r}.pt" for r in range(world)]
+
+
+@pytest.mark.parametrize("world", [1, 2])
+def test_slab_diffusion_checkpoint_resume_bit_identical(tmp_path, world):
+    out = tmp_path / "ok.npy"
+    mp.spawn(_ckpt_diff_worker, args=(world, _free_port(), (8, 6, 7), str(tmp_path / "df.{rank}.pt"), str(out)),
+             nprocs=world, join=True)
+    assert np.load(out).all()
+
+
+def test_checkpoint_rejects_mismatched_run(tmp_path):
+    """A shard checkpoint refuses to load into a different decomposition."""
+    from paper_2411_18889_b200.distributed import ShardedLeapfrog
+
+    sd = {"kind": "ShardedLeapfrog", "n_total": 512, "world": 2, "rank": 0}
+
+    class Fake:
+        plan = type("P", (), {"n_total": 256, "world": 1, "rank": 0})()
+        eps, dt = 0.1, 0.1
+
+    with pytest.raises(ValueError, match="checkpoint is for"):
+        ShardedLeapfrog.load_state_dict(Fake(), sd)
+    with pytest.raises(ValueError, match="not a ShardedLeapfrog"):
+        ShardedLeapfrog.load_state_dict(Fake(), {"kind": "Leapfrog"})

@@ -484,3 +484,30 @@ def test_leapfrog_persistent_small_n_bit_identical(tmp_path):
         res[flag] = np.load(dst)
     for k in res["0"].files:
         assert bits_equal(res["1"][k], res["0"][k]), k
+
+
+def test_checkpoint_resume_single_device(b2, tmp_path):
+    """Leapfrog (persistent small-N path) and Diffusion3D (resident path): N steps straight ==
+    k steps + save + fresh driver from the checkpoint + N-k steps, bit for bit."""
+    pos, vel = b2.plummer(4096, 3)
+    a = b2.Leapfrog(pos.clone(), vel.clone(), 2.0 ** -6, 2.0 ** -7)
+    a.step(6)
+    b = b2.Leapfrog(pos.clone(), vel.clone(), 2.0 ** -6, 2.0 ** -7)
+    b.step(4)
+    path = b2.save_checkpoint(b, tmp_path / "lf.pt")
+    c = b2.Leapfrog.from_state_dict(torch.load(path, weights_only=True))
+    c.step(2)
+    for x, y in ((a.pos, c.pos), (a.vel, c.vel), (a.acc, c.acc)):
+        assert bits_equal(x.cpu().numpy(), y.cpu().numpy())
+    assert c.steps == 6
+    f0 = b2.init_grid(64, 48, 64, seed=4)
+    args = (0.1, 0.1, 0.1, 1e-3, 1.0)
+    d = b2.Diffusion3D(f0.clone(), *args)
+    d.run(7)
+    e = b2.Diffusion3D(f0.clone(), *args)
+    e.run(3)
+    b2.save_checkpoint(e, tmp_path / "df.pt")
+    g = b2.Diffusion3D(torch.zeros_like(f0), *args)
+    b2.load_checkpoint(g, tmp_path / "df.pt")
+    g.run(4)
+    assert bits_equal(d.field.cpu().numpy(), g.field.cpu().numpy()) and g.steps == 7
