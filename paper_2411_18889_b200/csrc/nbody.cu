@@ -478,7 +478,7 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_leapfrog_small(const Small
   if (tid < I) {
     x = a.pos[i0 + tid];
     v = a.vel[i0 + tid];
-    acc = a.acc[i0 + tid];
+    if (!(a.flags & B2_INIT_ACC)) acc = a.acc[i0 + tid];  // else computed below (acc may be uninitialised)
   }
   const float2 e2 = make_float2(a.eps2, a.eps2);
   __syncthreads();

@@ -1,5 +1,6 @@
-SOLOMON_DIFF_DIRECT_MAXCELLS=0 python -m pytest tests/test_parity_gpu.py -x -q -k "temporal or config1 or golden or bit_identical" 2>&1 | tail -2
-for g in 256 512 1024; do for tb in 1 0; do SOLOMON_DIFF_TEMPORAL=$tb python -c "
+# Two-steps-per-pass (k_diffusion_tb2) vs one step per pass: bit-identity tests, then effective GLUPS.
+SOLOMON_DIFF_DIRECT_MAXCELLS=0 timeout 600 python -m pytest tests/test_parity_gpu.py -x -q -k "temporal or config1 or golden or bit_identical" 2>&1 | tail -2
+for g in 256 512 1024; do for tb in 1 0; do SOLOMON_DIFF_TEMPORAL=$tb timeout 300 python -c "
 import sys; sys.path.insert(0,'.')
 import torch, paper_2411_18889_b200 as b2
 g=$g; f = b2.init_grid(g,g,g); sim = b2.Diffusion3D(f, 1/g,1/g,1/g, 0.1/g**2); sim.run(4); torch.cuda.synchronize()

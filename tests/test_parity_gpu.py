@@ -302,8 +302,10 @@ def test_diffusion_run_temporal_blocking_bit_identical(b2, restatement, shape, s
     assert bits_equal(got, want)
 
 
-def test_temporal_blocking_kernel_opt_in_bit_identical(tmp_path):
-    """The opt-in 2-steps-per-pass kernel (SOLOMON_DIFF_TEMPORAL=1) in a fresh process."""
+def test_temporal_blocking_kernel_bit_identical(tmp_path):
+    """Two steps per HBM pass (k_diffusion_tb2: producer / step-1 / step-2 warps on mbarriers,
+    out-of-grid rows as edge copies) == single steps, bit for bit, on tile shapes with edge
+    tiles, ragged last tiles, i-splits and both parities; plus the forced single-step path."""
     import os
     import subprocess
     import sys
@@ -312,16 +314,18 @@ def test_temporal_blocking_kernel_opt_in_bit_identical(tmp_path):
         "import sys, numpy as np, torch; sys.path.insert(0, '.'); sys.path.insert(0, 'tests')\n"
         "import oracle, paper_2411_18889_b200 as b2\n"
         "args = (0.03, 0.02, 0.025, 2e-5, 1.0)\n"
-        "for shape, steps in [((40, 37, 128), 4), ((13, 9, 512), 5), ((256, 64, 512), 6), ((66, 30, 1024), 2)]:\n"
+        "for shape, steps in [((40, 37, 128), 4), ((13, 9, 512), 5), ((256, 64, 512), 6), ((66, 30, 1024), 2),\n"
+        "                     ((300, 70, 256), 3), ((19, 131, 512), 4), ((9, 512, 128), 7), ((64, 5, 512), 2)]:\n"
         "    f0 = np.random.default_rng(3).random(shape, dtype=np.float32)\n"
         "    want = oracle.Restatement().diffusion_run(f0, steps, *args)\n"
         "    got = b2.Diffusion3D(torch.from_numpy(f0).cuda(), *args).run(steps).cpu().numpy()\n"
         "    assert np.array_equal(got.view(np.uint32), want.view(np.uint32)), shape\n"
         "print('ok')\n")
-    env = dict(os.environ, SOLOMON_DIFF_TEMPORAL="1", SOLOMON_DIFF_DIRECT_MAXCELLS="0")
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    out = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True)
-    assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-2000:]
+    for tb in ("1", "0"):
+        env = dict(os.environ, SOLOMON_DIFF_TEMPORAL=tb, SOLOMON_DIFF_DIRECT_MAXCELLS="0", SOLOMON_DIFF_RESIDENT="0")
+        out = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True)
+        assert out.returncode == 0 and "ok" in out.stdout, (tb, out.stderr[-2000:])
 
 
 def test_dropin_edge_cases(b2, golden, restatement):
