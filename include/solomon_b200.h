@@ -148,9 +148,9 @@ int b2_diffusion3d_slab(int nx_local, int ny, int nz, float dx, float dy, float 
  * Grids that fit the chip's shared memory (e.g. 128^3) run all steps in one
  * persistent launch with the field resident in shared memory (bricks
  * exchanging faces through a library-owned mailbox); other L2-resident grids
- * in one cooperative launch; large grids one HBM pass per step
- * (SOLOMON_DIFF_TEMPORAL=1 opts into the experimental two-steps-per-pass
- * kernel). All paths are bit-identical to nsteps single steps.
+ * in one cooperative launch; large grids two steps per HBM pass where the
+ * planner finds a worthwhile tile (SOLOMON_DIFF_TEMPORAL=0: one step per
+ * pass). All paths are bit-identical to nsteps single steps.
  * *result_in_fn (if not NULL) is set to 1 when the final field is in fn, 0
  * when it is in f; the other buffer is scratch. */
 int b2_diffusion3d_run(int nx, int ny, int nz, float dx, float dy, float dz, float dt, float kappa,
