@@ -18,10 +18,14 @@ KEEP = {
     "k_diffusion_march": ["gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
                           "sm__warps_active.avg.pct_of_peak_sustained_active",
                           "smsp__issue_active.avg.pct_of_peak_sustained_active"],
+    "k_diffusion_tb2": ["gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
+                        "smsp__issue_active.avg.pct_of_peak_sustained_active",
+                        "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed"],
 }
 NOTES = {
     "k_force_fast": "N=2^20, 64 j-chunks: DRAM traffic is the 1 GiB partial-sum write; FP32-pipe (register-file) bound",
     "k_diffusion_march": "512^3 step under ncu replay (cold L2); algorithmic 1.074 GB (8 B/cell)",
+    "k_diffusion_tb2": "512^3, one launch = two steps, under ncu replay; algorithmic 1.074 GB (8 B/cell per launch)",
 }
 
 
