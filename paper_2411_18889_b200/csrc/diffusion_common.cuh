@@ -1,0 +1,126 @@
+// Shared pieces of the diffusion kernels: the reference arithmetic and coefficients
+// (listing_diffusion.c:6-21), PTX helpers (mbarrier, bulk async copy), and the entry
+// points the time-loop dispatcher in diffusion.cu calls into diffusion_tb2.cu and
+// diffusion_resident.cu.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstddef>
+#include <cstdint>
+#include <cstdlib>
+
+#include "common.cuh"
+
+namespace b2 {
+
+struct Coefs {
+  float cc, ce, cn, ct;
+};
+
+// listing_diffusion.c:6-9, evaluated in the same order as the reference build.
+inline Coefs make_coefs(float dx, float dy, float dz, float dt, float kappa) {
+  volatile float kd = kappa * dt;  // volatile: keep every FP32 rounding on the host too
+  volatile float ce = kd / (dx * dx);
+  volatile float cn = kd / (dy * dy);
+  volatile float ct = kd / (dz * dz);
+  volatile float s = ce + ce;
+  s = s + cn;
+  s = s + cn;
+  s = s + ct;
+  s = s + ct;
+  Coefs c;
+  c.cc = 1.0f - s;
+  c.ce = ce;
+  c.cn = cn;
+  c.ct = ct;
+  return c;
+}
+
+__device__ __forceinline__ float cell(const Coefs& c, float fc, float fip, float fim, float fjp, float fjm, float fkp,
+                                      float fkm) {
+  float v = __fmul_rn(c.ce, fip);
+  v = __fmaf_rn(c.cc, fc, v);
+  v = __fmaf_rn(c.ce, fim, v);  // cw = ce
+  v = __fmaf_rn(c.cn, fjp, v);
+  v = __fmaf_rn(c.cn, fjm, v);  // cs = cn
+  v = __fmaf_rn(c.ct, fkp, v);
+  v = __fmaf_rn(c.ct, fkm, v);  // cb = ct
+  return v;
+}
+
+// Four consecutive-k cells at once with packed FP32 (FFMA2/FMUL2: per-lane IEEE
+// fma/mul, so identical to four cell() calls) -- halves the FP32 issue slots of
+// the stencil arithmetic. kl = f[k0-1] (clamped), kr = f[k0+4] (clamped).
+__device__ __forceinline__ float4 cell4(const Coefs& c, float4 fc, float4 fip, float4 fim, float4 fjp, float4 fjm,
+                                        float kl, float kr) {
+  const float2 ce = make_float2(c.ce, c.ce), cc = make_float2(c.cc, c.cc);
+  const float2 cn = make_float2(c.cn, c.cn), ct = make_float2(c.ct, c.ct);
+  float2 lo = __fmul2_rn(ce, make_float2(fip.x, fip.y));
+  float2 hi = __fmul2_rn(ce, make_float2(fip.z, fip.w));
+  lo = __ffma2_rn(cc, make_float2(fc.x, fc.y), lo);
+  hi = __ffma2_rn(cc, make_float2(fc.z, fc.w), hi);
+  lo = __ffma2_rn(ce, make_float2(fim.x, fim.y), lo);
+  hi = __ffma2_rn(ce, make_float2(fim.z, fim.w), hi);
+  lo = __ffma2_rn(cn, make_float2(fjp.x, fjp.y), lo);
+  hi = __ffma2_rn(cn, make_float2(fjp.z, fjp.w), hi);
+  lo = __ffma2_rn(cn, make_float2(fjm.x, fjm.y), lo);
+  hi = __ffma2_rn(cn, make_float2(fjm.z, fjm.w), hi);
+  lo = __ffma2_rn(ct, make_float2(fc.y, fc.z), lo);  // f[k+1]
+  hi = __ffma2_rn(ct, make_float2(fc.w, kr), hi);
+  lo = __ffma2_rn(ct, make_float2(kl, fc.x), lo);    // f[k-1]
+  hi = __ffma2_rn(ct, make_float2(fc.y, fc.z), hi);
+  return make_float4(lo.x, lo.y, hi.x, hi.y);
+}
+
+// ---- PTX helpers: mbarrier + bulk async copy (sm_90+/sm_100a) -------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+__device__ __forceinline__ void st_stream(float4* p, float4 v) { __stcs(p, v); }
+
+inline int env_int(const char* name, int dflt) {  // tuning knobs for bench sweeps
+  const char* e = std::getenv(name);
+  return e ? std::atoi(e) : dflt;
+}
+
+// ---- two steps per HBM pass (diffusion_tb2.cu) ----
+constexpr int kTBStages = 4;  // input-ring and step-1-ring depth (powers of two: slot math is masks)
+struct TB2Plan {
+  int TJ = 0, S1 = 0, S2 = 0, nst = kTBStages, ns1 = kTBStages, n_jtiles = 0, IC = 0, grid = 0, R = 0, R1 = 0;
+  size_t smem = 0;
+};
+bool plan_tb2(int nx, int ny, int nz, TB2Plan& best);
+int launch_tb2(const TB2Plan& p, int nx, int ny, int nz, const Coefs& c, const float* f, float* fn, cudaStream_t s);
+
+// ---- shared-memory-resident time loop (diffusion_resident.cu) ----
+// Launches all nsteps for grids that fit the SMs' shared memory; false if not applicable.
+bool launch_resident(int nx, int ny, int nz, const Coefs& c, float* f, float* fn, int nsteps, cudaStream_t s);
+
+}  // namespace b2

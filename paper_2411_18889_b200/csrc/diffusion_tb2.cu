@@ -1,0 +1,307 @@
+// K3' -- two explicit diffusion steps per HBM pass (temporal blocking), for the
+// device-resident time loop b2_diffusion3d_run on large grids. Reference arithmetic:
+// pkg/tests/fixtures/listing_diffusion.c:5-25 via cell4 (diffusion_common.cuh).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstddef>
+#include <cstdint>
+
+#include "diffusion_common.cuh"
+
+namespace b2 {
+
+// ---------------------------------------------------------------------------
+// Two steps per HBM pass (temporal blocking) for the device-resident time loop
+// (b2_diffusion3d_run), warp-specialised. A CTA owns output rows [j0, j0+TJ)
+// of step 2 over planes [i0, i1) and marches along i as a three-role pipeline
+// coupled only by mbarriers (no CTA-wide barrier in the loop):
+//
+//   producer warp  -- cp.async.bulk of input rows j0-2 .. j0-2+R-1 of each plane
+//                     into an NST-deep ring (full/empty mbarriers). Rows outside
+//                     the grid are filled with copies of the edge row, so the
+//                     j clamp of listing_diffusion.c:17-18 is in the data;
+//   step-1 warps   -- step 1 on rows j0-1 .. (one row each side recomputed, as
+//                     the neighbour tile does) into an NS1-deep ring of step-1
+//                     planes; the edge rows are also stored into the row just
+//                     outside the grid (the clamp for step 2);
+//   step-2 warps   -- step 2 on rows [j0, j0+TJ) from the step-1 ring, one plane
+//                     behind, streamed to fn with evict-first stores.
+//
+// Each compute thread owns one float4 column and S consecutive rows, with the
+// i-1 / i values in registers: the in-plane j neighbours are its own registers
+// except at its block ends, so a cell costs one LDS.128 (i+1), two LDS.32 (k+-1)
+// and the 14 packed-FP32 ops. f is read once and f'' written once: 8 B of HBM
+// per two cell-updates. Arithmetic and clamps as two single steps: bit-identical.
+struct TB2Args {
+  const float* f;
+  float* fn;
+  int nx, ny, nz;
+  int TJ, n_jtiles, IC, nst, ns1;
+  int R, R1;  // rows per input-ring slot / per step-1 slot
+  Coefs c;
+};
+
+constexpr int kTBWarps1 = 8, kTBWarps2 = 8;
+constexpr int kTBThreads = 32 * (1 + kTBWarps1 + kTBWarps2);
+// Every compute thread arrives on the ring mbarriers itself (release of its own
+// shared-memory accesses): measured as fast as one elected lane per warp after
+// __syncwarp, and clean under compute-sanitizer racecheck.
+constexpr int kTBArrive = 32;
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+template <int S1, int S2>
+__global__ void __launch_bounds__(kTBThreads, 1) k_diffusion_tb2(const TB2Args a) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const int nz = a.nz, nz4 = nz >> 2, ny = a.ny, nx = a.nx;
+  const int TJ = a.TJ;
+  constexpr int NST = kTBStages, NS1 = kTBStages;
+  const size_t plane = static_cast<size_t>(ny) * nz;
+  const int in_floats = a.R * nz;   // ring row r <-> global row j0 - 2 + r
+  const int s1_floats = a.R1 * nz;  // s1 row r <-> global row j0 - 1 + r
+
+  uint64_t* full_in = reinterpret_cast<uint64_t*>(smem_raw);
+  uint64_t* empty_in = full_in + NST;
+  uint64_t* full_s1 = empty_in + NST;
+  uint64_t* empty_s1 = full_s1 + NS1;
+  float* in_ring = reinterpret_cast<float*>(smem_raw + 256);
+  float* s1_ring = in_ring + static_cast<size_t>(NST) * in_floats;
+
+  const int jt = blockIdx.x % a.n_jtiles, ic = blockIdx.x / a.n_jtiles;
+  const int j0 = jt * TJ, rows = min(TJ, ny - j0);
+  const int i0 = ic * a.IC, i1 = min(i0 + a.IC, nx);
+  if (i0 >= i1) return;                                               // uniform per CTA
+  const int qlo = max(i0 - 1, 0), qhi = min(i1, nx - 1);              // step-1 planes
+  const int lo_in = max(qlo - 1, 0), hi_in = min(qhi + 1, nx - 1);    // input planes
+  const int L = hi_in - lo_in + 1;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  if (threadIdx.x == 0) {
+    for (int k = 0; k < NST; ++k) {
+      mbar_init(full_in + k, 1);
+      mbar_init(empty_in + k, kTBArrive * kTBWarps1);
+    }
+    for (int k = 0; k < NS1; ++k) {
+      mbar_init(full_s1 + k, kTBArrive * kTBWarps1);
+      mbar_init(empty_s1 + k, kTBArrive * kTBWarps2);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  if (warp == 0) {  // ---- producer ----
+    if (lane == 0) {
+      const int R = a.R;
+      const int gfirst = max(j0 - 2, 0), glast = min(j0 - 2 + R - 1, ny - 1);
+      const uint32_t row_bytes = static_cast<uint32_t>(nz * sizeof(float));
+      const uint32_t main_bytes = static_cast<uint32_t>(glast - gfirst + 1) * row_bytes;
+      const int n_top = gfirst - (j0 - 2), n_bot = (j0 - 2 + R - 1) - glast;  // rows outside the grid
+      const uint32_t bytes = main_bytes + static_cast<uint32_t>(n_top + n_bot) * row_bytes;
+      for (int t = 0; t < L; ++t) {
+        const int st = t % NST;
+        if (t >= NST) mbar_wait(empty_in + st, ((t / NST) - 1) & 1);
+        fence_proxy_async();  // generic reads of the slot before the async-proxy refill
+        mbar_expect_tx(full_in + st, bytes);
+        float* slot = in_ring + static_cast<size_t>(st) * in_floats;
+        const float* src = a.f + static_cast<size_t>(lo_in + t) * plane;
+        bulk_g2s(slot + n_top * nz, src + static_cast<size_t>(gfirst) * nz, main_bytes, full_in + st);
+        for (int r = 0; r < n_top; ++r) bulk_g2s(slot + r * nz, src, row_bytes, full_in + st);  // IMAX(j-1, 0)
+        for (int r = 0; r < n_bot; ++r)                                                         // IMIN(j+1, ny-1)
+          bulk_g2s(slot + (R - 1 - r) * nz, src + static_cast<size_t>(ny - 1) * nz, row_bytes, full_in + st);
+      }
+    }
+    return;
+  }
+
+  const Coefs c = a.c;
+  auto s1_slot = [&](int q) { return s1_ring + static_cast<size_t>((q - qlo) % NS1) * s1_floats; };
+  auto wait_s1 = [&](int q) { const int t = q - qlo; mbar_wait(full_s1 + t % NS1, (t / NS1) & 1); };
+
+  if (warp <= kTBWarps1) {  // ---- step 1: s1 rows r = 0 .. <-> global j0-1+r (ring row r+1) ----
+    const int tid = threadIdx.x - 32;
+    auto in_slot = [&](int pl) { return in_ring + static_cast<size_t>((pl - lo_in) % NST) * in_floats; };
+    auto wait_in = [&](int pl) { const int t = pl - lo_in; mbar_wait(full_in + t % NST, (t / NST) & 1); };
+    const int c4 = tid % nz4, r0 = (tid / nz4) * S1;
+    const bool kfirst = c4 == 0, klast = c4 + 1 == nz4;
+    unsigned int real = 0, dup_up = 0, dup_dn = 0;  // bit k: row inside the grid / also store at row-1 / row+1
+#pragma unroll
+    for (int k = 0; k < S1; ++k) {
+      const int g = j0 - 1 + r0 + k;
+      if (g >= 0 && g < ny) real |= 1u << k;
+      if (g == 0 && r0 + k >= 1) dup_up |= 1u << k;               // s1 row for g = -1 := s1(g = 0)
+      if (g == ny - 1 && r0 + k + 1 < a.R1) dup_dn |= 1u << k;    // s1 row for g = ny := s1(g = ny-1)
+    }
+    const int base = (r0 + 1) * nz + 4 * c4;  // ring offset of row r0; s1 offset of row r0 is base - nz
+    float4 xp[S1], xc[S1];
+    if (qlo > 0) {
+      wait_in(qlo - 1);
+      const float* b = in_slot(qlo - 1) + base;
+#pragma unroll
+      for (int k = 0; k < S1; ++k) xp[k] = *reinterpret_cast<const float4*>(b + k * nz);
+    }
+    wait_in(qlo);
+    {
+      const float* b = in_slot(qlo) + base;
+#pragma unroll
+      for (int k = 0; k < S1; ++k) {
+        xc[k] = *reinterpret_cast<const float4*>(b + k * nz);
+        if (qlo == 0) xp[k] = xc[k];  // IMAX(i-1, 0)
+      }
+    }
+    if (qlo > 0) mbar_arrive(empty_in + (qlo - 1 - lo_in) % NST);
+    for (int q = qlo; q <= qhi; ++q) {
+      const bool has_next = q + 1 <= nx - 1;
+      if (has_next) wait_in(q + 1);
+      const int t1 = q - qlo;
+      if (t1 >= NS1) mbar_wait(empty_s1 + t1 % NS1, ((t1 / NS1) - 1) & 1);
+      const float* __restrict__ cur = in_slot(q) + base;
+      const float* __restrict__ nxt = has_next ? in_slot(q + 1) + base : cur;  // IMIN(i+1, nx-1)
+      float* __restrict__ out = s1_slot(q) + base - nz;
+#pragma unroll
+      for (int k = 0; k < S1; ++k) {
+        const float* rowp = cur + k * nz;
+        const float4 xn = *reinterpret_cast<const float4*>(nxt + k * nz);
+        const float4 fjp = k + 1 < S1 ? xc[k + 1] : *reinterpret_cast<const float4*>(rowp + nz);
+        const float4 fjm = k > 0 ? xp[k - 1] : *reinterpret_cast<const float4*>(rowp - nz);  // xp[k-1]: old xc[k-1]
+        const float kl = kfirst ? xc[k].x : rowp[-1];  // IMAX(k-1, 0)
+        const float kr = klast ? xc[k].w : rowp[4];    // IMIN(k+1, nz-1)
+        const float4 o = cell4(c, xc[k], xn, xp[k], fjp, fjm, kl, kr);
+        float* dst = out + k * nz;
+        if (real >> k & 1) *reinterpret_cast<float4*>(dst) = o;
+        if (dup_up >> k & 1) *reinterpret_cast<float4*>(dst - nz) = o;
+        if (dup_dn >> k & 1) *reinterpret_cast<float4*>(dst + nz) = o;
+        xp[k] = xc[k];
+        xc[k] = xn;
+      }
+      mbar_arrive(full_s1 + t1 % NS1);
+      mbar_arrive(empty_in + (q - lo_in) % NST);
+    }
+    return;
+  }
+
+  // ---- step 2: output rows j0 + r2 (s1 row r2 + 1) ----
+  const int tid = threadIdx.x - 32 * (1 + kTBWarps1);
+  const int c4 = tid % nz4, r0 = (tid / nz4) * S2;
+  const bool kfirst = c4 == 0, klast = c4 + 1 == nz4;
+  unsigned int comp = 0;
+#pragma unroll
+  for (int k = 0; k < S2; ++k)
+    if (r0 + k < rows) comp |= 1u << k;
+  const int base = (r0 + 1) * nz + 4 * c4;  // s1 offset of row r0
+  float4 ya[S2], yb[S2];
+  if (i0 > 0) {
+    wait_s1(i0 - 1);
+    const float* b = s1_slot(i0 - 1) + base;
+#pragma unroll
+    for (int k = 0; k < S2; ++k) ya[k] = *reinterpret_cast<const float4*>(b + k * nz);
+  }
+  wait_s1(i0);
+  {
+    const float* b = s1_slot(i0) + base;
+#pragma unroll
+    for (int k = 0; k < S2; ++k) {
+      yb[k] = *reinterpret_cast<const float4*>(b + k * nz);
+      if (i0 == 0) ya[k] = yb[k];  // IMAX(i-1, 0) on step-1 values
+    }
+  }
+  if (i0 > 0) {
+    mbar_arrive(empty_s1 + (i0 - 1 - qlo) % NS1);
+  }
+  for (int p = i0; p < i1; ++p) {
+    const bool has_next = p + 1 <= nx - 1;
+    if (has_next) wait_s1(p + 1);
+    const float* __restrict__ cur = s1_slot(p) + base;
+    const float* __restrict__ nxt = has_next ? s1_slot(p + 1) + base : cur;  // IMIN(i+1, nx-1)
+    // output row g = j0 + r0 + k = j0 - 1 + (s1 row): fn offset = s1 offset + (j0 - 1) * nz
+    float* dst = a.fn + static_cast<ptrdiff_t>(p) * static_cast<ptrdiff_t>(plane) +
+                 static_cast<ptrdiff_t>(j0 - 1) * nz + base;
+#pragma unroll
+    for (int k = 0; k < S2; ++k) {
+      const float* rowp = cur + k * nz;
+      const float4 yn = *reinterpret_cast<const float4*>(nxt + k * nz);
+      const float4 fjp = k + 1 < S2 ? yb[k + 1] : *reinterpret_cast<const float4*>(rowp + nz);
+      const float4 fjm = k > 0 ? ya[k - 1] : *reinterpret_cast<const float4*>(rowp - nz);  // ya[k-1]: old yb[k-1]
+      const float kl = kfirst ? yb[k].x : rowp[-1];
+      const float kr = klast ? yb[k].w : rowp[4];
+      if (comp >> k & 1) st_stream(reinterpret_cast<float4*>(dst + k * nz), cell4(c, yb[k], yn, ya[k], fjp, fjm, kl, kr));
+      ya[k] = yb[k];
+      yb[k] = yn;
+    }
+    mbar_arrive(empty_s1 + (p - qlo) % NS1);
+  }
+}
+
+// Temporal-blocked (2 steps per pass) plan for k_diffusion_tb2: one CTA per SM
+// (~170 KB of rings), TJ output rows per tile chosen so that j-tiles x i-splits
+// fill the SMs in one wave while keeping the recomputed halo rows (2 of TJ+2)
+// small; S1/S2 = float4 cells per step-1/step-2 thread must match an
+// instantiation below.
+
+static bool tb2_instantiated(int S1, int S2) {
+  return (S1 == 2 && (S2 == 1 || S2 == 2)) || (S1 == 3 && (S2 == 2 || S2 == 3)) ||
+         (S1 == 4 && (S2 == 3 || S2 == 4)) || (S1 == 5 && (S2 == 3 || S2 == 4)) || (S1 == 6 && (S2 == 5 || S2 == 6));
+}
+
+bool plan_tb2(int nx, int ny, int nz, TB2Plan& best) {
+  if (nz % 4 != 0 || nx < 2) return false;
+  const int nz4 = nz / 4;
+  if ((32 * kTBWarps1) % nz4 != 0 || (32 * kTBWarps2) % nz4 != 0 || nz4 < 32) return false;  // row blocks, full warps
+  const int blocks1 = 32 * kTBWarps1 / nz4, blocks2 = 32 * kTBWarps2 / nz4;
+  const DeviceInfo& di = device_info();
+  const size_t cap = static_cast<size_t>(di.smem_optin > 0 ? di.smem_optin : 227 * 1024);
+  static const int force_tj = env_int("SOLOMON_DIFF_TB_TJ", 0);  // tuning knob (scripts/tb.sh sweeps)
+  double best_score = -1.0;
+  for (int TJ = 1; TJ <= std::min(ny, 32); ++TJ) {
+    if (force_tj && TJ != force_tj) continue;
+    TB2Plan p;
+    p.TJ = TJ;
+    p.S1 = (TJ + 2 + blocks1 - 1) / blocks1;
+    p.S2 = (TJ + blocks2 - 1) / blocks2;
+    if (!tb2_instantiated(p.S1, p.S2) || TJ < 5) continue;  // TJ < 5: recomputed halo rows cost more than they save
+    p.R1 = std::max(blocks1 * p.S1, blocks2 * p.S2 + 2);  // step-1 rows written / read (one past the last)
+    p.R = blocks1 * p.S1 + 2;                             // input rows read by step 1
+    p.smem = 256 + (static_cast<size_t>(p.nst) * p.R + static_cast<size_t>(p.ns1) * p.R1) * nz * sizeof(float);
+    if (p.smem > cap) continue;
+    p.n_jtiles = (ny + TJ - 1) / TJ;
+    const int splits = std::max(1, std::min(di.sms / p.n_jtiles, std::max(1, nx / 8)));
+    p.IC = (nx + splits - 1) / splits;
+    p.grid = p.n_jtiles * ((nx + p.IC - 1) / p.IC);
+    const double waves = std::ceil(static_cast<double>(p.grid) / di.sms);
+    const double util = p.grid / (waves * di.sms);
+    const double score = util * TJ / (TJ + 2.0) * static_cast<double>(p.IC) / (p.IC + 2.0);
+    if (score > best_score) {
+      best_score = score;
+      best = p;
+    }
+  }
+  return best_score > 0;
+}
+
+template <int S1, int S2>
+static void launch_tb2_t(const TB2Plan& p, const TB2Args& a, cudaStream_t s) {
+  static bool set[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (!set[dev]) {  // per device: the opt-in is a per-context function attribute
+    cudaFuncSetAttribute(k_diffusion_tb2<S1, S2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    set[dev] = true;
+  }
+  k_diffusion_tb2<S1, S2><<<p.grid, kTBThreads, p.smem, s>>>(a);
+}
+
+int launch_tb2(const TB2Plan& p, int nx, int ny, int nz, const Coefs& c, const float* f, float* fn,
+                      cudaStream_t s) {
+  TB2Args a{f, fn, nx, ny, nz, p.TJ, p.n_jtiles, p.IC, p.nst, p.ns1, p.R, p.R1, c};
+#define B2_TB2_CASE(A, B) \
+  if (p.S1 == A && p.S2 == B) launch_tb2_t<A, B>(p, a, s); else
+  B2_TB2_CASE(2, 1) B2_TB2_CASE(2, 2) B2_TB2_CASE(3, 2) B2_TB2_CASE(3, 3) B2_TB2_CASE(4, 3) B2_TB2_CASE(4, 4)
+  B2_TB2_CASE(5, 3) B2_TB2_CASE(5, 4) B2_TB2_CASE(6, 5) B2_TB2_CASE(6, 6) return B2_EINVAL;
+#undef B2_TB2_CASE
+  return launch_status();
+}
+
+}  // namespace b2

@@ -8,7 +8,7 @@
 // the neighbours' tagged faces), march, face export, and
 // the whole step.
 #define B2_RESIDENT_TRACE
-#include "../paper_2411_18889_b200/csrc/diffusion.cu"
+#include "../paper_2411_18889_b200/csrc/diffusion_resident.cu"
 
 #include <cstdio>
 #include <vector>
