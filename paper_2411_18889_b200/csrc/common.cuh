@@ -24,6 +24,10 @@ struct DeviceInfo {
 };
 const DeviceInfo& device_info();
 
+// Opt the kernel `fn` into the full dynamic shared memory of the current device,
+// once per (device, kernel) -- the attribute is per context. Thread-safe.
+void allow_max_dynamic_smem(const void* fn);
+
 // ---- Device helpers shared by the persistent kernels (k_leapfrog_small,
 // k_diffusion_resident): 16-byte words a producer CTA publishes and a consumer
 // CTA polls. A .b128 access is single-copy atomic (PTX memory model; libcu++'s

@@ -332,17 +332,11 @@ static int launch_step(int nx, int ny, int nz, const Coefs& c, const float* f, c
   if (ok_align && plan_march(i_end - i_begin, ny, nz, mp)) {
     MarchArgs a{f, lo, hi, fn, nx, ny, nz, mp.TJ, mp.n_jtiles, i_begin, i_end, mp.IC, mp.nst, c};
     switch (mp.S) {
-#define B2_MARCH_CASE(SV)                                                                                     \
-  case SV: {                                                                                                  \
-    static bool attr_set[64] = {};                                                                            \
-    int dev_ = 0;                                                                                             \
-    cudaGetDevice(&dev_);                                                                                     \
-    if (!attr_set[dev_]) {                                                                                    \
-      cudaFuncSetAttribute(k_diffusion_march<SV>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024); \
-      attr_set[dev_] = true;                                                                                  \
-    }                                                                                                         \
-    k_diffusion_march<SV><<<mp.grid, kMarchThreads, mp.smem, s>>>(a);                                         \
-    break;                                                                                                    \
+#define B2_MARCH_CASE(SV)                                                       \
+  case SV: {                                                                    \
+    allow_max_dynamic_smem(reinterpret_cast<const void*>(k_diffusion_march<SV>)); \
+    k_diffusion_march<SV><<<mp.grid, kMarchThreads, mp.smem, s>>>(a);           \
+    break;                                                                      \
   }
       B2_MARCH_CASE(1)
       B2_MARCH_CASE(2)

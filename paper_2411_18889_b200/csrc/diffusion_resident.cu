@@ -312,14 +312,10 @@ bool launch_resident(int nx, int ny, int nz, const Coefs& c, float* f, float* fn
   const int nbricks = p.nbi * p.nbj;
   static std::mutex mu;
   static Mailbox boxes[64];
-  static bool attr[64] = {};
+  allow_max_dynamic_smem(reinterpret_cast<const void*>(k_diffusion_resident));
   int dev = 0;
   cudaGetDevice(&dev);
   std::lock_guard<std::mutex> lk(mu);
-  if (!attr[dev]) {
-    cudaFuncSetAttribute(k_diffusion_resident, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    attr[dev] = true;
-  }
   int per_sm = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_diffusion_resident, kResidentThreads, p.smem) !=
           cudaSuccess ||

@@ -283,13 +283,7 @@ bool plan_tb2(int nx, int ny, int nz, TB2Plan& best) {
 
 template <int S1, int S2>
 static void launch_tb2_t(const TB2Plan& p, const TB2Args& a, cudaStream_t s) {
-  static bool set[64] = {};
-  int dev = 0;
-  cudaGetDevice(&dev);
-  if (!set[dev]) {  // per device: the opt-in is a per-context function attribute
-    cudaFuncSetAttribute(k_diffusion_tb2<S1, S2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    set[dev] = true;
-  }
+  allow_max_dynamic_smem(reinterpret_cast<const void*>(k_diffusion_tb2<S1, S2>));
   k_diffusion_tb2<S1, S2><<<p.grid, kTBThreads, p.smem, s>>>(a);
 }
 

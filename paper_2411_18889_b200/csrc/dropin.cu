@@ -40,6 +40,18 @@ const DeviceInfo& device_info() {
   return infos[dev];
 }
 
+void allow_max_dynamic_smem(const void* fn) {
+  static std::mutex mu;
+  static std::vector<std::pair<int, const void*>> done;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(mu);
+  for (const auto& d : done)
+    if (d.first == dev && d.second == fn) return;
+  cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, device_info().smem_optin);
+  done.emplace_back(dev, fn);
+}
+
 // Per-device staging arena for host-pointer calls (grown on demand, never shrunk).
 struct Arena {
   void* ptr = nullptr;

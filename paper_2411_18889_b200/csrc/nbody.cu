@@ -701,13 +701,7 @@ static bool launch_leapfrog_small(int n, float4* pos, float4* vel, float4* acc, 
   const bool pot = flags & B2_POTENTIAL;
   const void* fn = pot ? reinterpret_cast<const void*>(k_leapfrog_small<true>)
                        : reinterpret_cast<const void*>(k_leapfrog_small<false>);
-  static bool attr[64][2] = {};
-  int dev = 0;
-  cudaGetDevice(&dev);
-  if (!attr[dev][pot]) {
-    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    attr[dev][pot] = true;
-  }
+  allow_max_dynamic_smem(fn);
   int per_sm = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kSmallThreads, smem) != cudaSuccess ||
       per_sm * di.sms < ctas) {
