@@ -22,6 +22,9 @@ const DeviceInfo& device_info() {
   }
   return d;
 }
+void allow_max_dynamic_smem(const void* fn) {
+  cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, device_info().smem_optin);
+}
 }  // namespace b2
 
 int main(int argc, char** argv) {

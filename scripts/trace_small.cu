@@ -7,7 +7,7 @@
 // prints the mean duration of: gather (incl. waiting for other CTAs' positions),
 // force + reduce, kick/drift/publish, and the whole step.
 #define B2_SMALL_TRACE
-#include "../paper_2411_18889_b200/csrc/nbody.cu"
+#include "../paper_2411_18889_b200/csrc/nbody_small.cu"
 
 #include <cstdio>
 #include <vector>
@@ -20,6 +20,9 @@ const DeviceInfo& device_info() {
     cudaDeviceGetAttribute(&d.smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, 0);
   }
   return d;
+}
+void allow_max_dynamic_smem(const void* fn) {
+  cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, device_info().smem_optin);
 }
 }  // namespace b2
 
