@@ -244,3 +244,73 @@ def test_checkpoint_rejects_mismatched_run(tmp_path):
         ShardedLeapfrog.load_state_dict(Fake(), sd)
     with pytest.raises(ValueError, match="not a ShardedLeapfrog"):
         ShardedLeapfrog.load_state_dict(Fake(), {"kind": "Leapfrog"})
+
+
+def _random_cases_worker(rank, world, port, out_path):
+    """Seeded random cases inside one process group (the reference's seeded property-test style,
+    pkg/tests/test_acceptance.py:136-206): ragged slab splits, N not a power of two, runs left
+    open and closed -- each compared bit for bit with the unsharded computation on rank 0."""
+    _init(rank, world, port)
+    import random
+
+    import oracle
+    from paper_2411_18889_b200.distributed import ShardedLeapfrog, SlabDiffusion
+    from paper_2411_18889_b200.nbody import plummer_numpy
+
+    o = oracle.Restatement()
+    rnd = random.Random(987654321)
+    ok = True
+    for _ in range(6):  # n-body
+        n = world * rnd.randint(8, 96)
+        steps, chunk, close = rnd.randint(1, 4), rnd.choice([16, 64, 100]), rnd.random() < 0.5
+        pos, vel = plummer_numpy(n, rnd.randint(0, 1000))
+        nl = n // world
+        sim = ShardedLeapfrog(torch.from_numpy(pos[rank * nl:(rank + 1) * nl]),
+                              torch.from_numpy(vel[rank * nl:(rank + 1) * nl]), 2.0 ** -6, 2.0 ** -7,
+                              kernels=OracleNBodyKernels(chunk))
+        sim.step(steps, close=close)
+        gp = [torch.empty_like(sim.pos) for _ in range(world)]
+        gv = [torch.empty_like(sim.vel) for _ in range(world)]
+        dist.all_gather(gp, sim.pos.clone())
+        dist.all_gather(gv, sim.vel)
+        if rank == 0:
+            # unsharded, same chunked structure: init acc, open, (force, update) x steps
+            p, v = pos.copy(), vel.copy()
+            a = np.empty_like(p)
+            nch = (n + chunk - 1) // chunk
+            part = np.empty((nch * n, 4), np.float32)
+            h = 0.5 * 2.0 ** -7
+            o.calc_acc_partials(p, p, 2.0 ** -6, chunk, out=part)
+            o.kdk_update(None, None, a, part, nch, 0.0, 0.0, 0.0, 1)
+            o.kdk_update(p, v, a, None, nch, 0.0, h, 2.0 ** -7, 4)
+            for s in range(steps):
+                o.calc_acc_partials(p, p, 2.0 ** -6, chunk, out=part)
+                last = close and s + 1 == steps
+                o.kdk_update(p, v, a, part, nch, h, h, 2.0 ** -7, 1 | 2 | (0 if last else 4))
+            ok &= np.array_equal(torch.cat(gp).numpy().view(np.uint32), p.view(np.uint32))
+            ok &= np.array_equal(torch.cat(gv).numpy().view(np.uint32), v.view(np.uint32))
+    for _ in range(6):  # diffusion, ragged slabs
+        counts = [rnd.randint(2, 6) for _ in range(world)]
+        shape = (sum(counts), rnd.randint(1, 7), rnd.randint(1, 9))
+        steps = rnd.randint(1, 5)
+        args = (0.11, 0.07, 0.13, 1e-3, 1.0)
+        f0 = np.random.default_rng(rnd.randint(0, 1000)).random(shape, dtype=np.float32)
+        lo = sum(counts[:rank])
+        sim = SlabDiffusion(torch.from_numpy(f0[lo:lo + counts[rank]].copy()), *args,
+                            kernels=OracleSlabKernels(*args))
+        sim.step(steps)
+        parts = [None] * world
+        dist.all_gather_object(parts, sim.f.numpy())
+        if rank == 0:
+            want = o.diffusion_run(f0, steps, *args)
+            ok &= np.array_equal(np.concatenate(parts, axis=0).view(np.uint32), want.view(np.uint32))
+    if rank == 0:
+        np.save(out_path, np.array([ok]))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_drivers_random_cases(tmp_path, world):
+    out = tmp_path / "ok.npy"
+    mp.spawn(_random_cases_worker, args=(world, _free_port(), str(out)), nprocs=world, join=True)
+    assert np.load(out).all()
