@@ -7,6 +7,7 @@
 #include <cmath>
 #include <cstddef>
 #include <cstdint>
+#include <type_traits>
 
 #include "diffusion_common.cuh"
 
@@ -153,7 +154,11 @@ __global__ void __launch_bounds__(kTBThreads, 1) k_diffusion_tb2(const TB2Args a
       }
     }
     if (qlo > 0) mbar_arrive(empty_in + (qlo - 1 - lo_in) % NST);
-    for (int q = qlo; q <= qhi; ++q) {
+    // One step-1 plane; EDGE: this thread's rows include rows outside the grid or edge
+    // duplicates to store (tiles at j = 0 / ny-1 only) -- interior threads take the
+    // unpredicated copy (+4% at 512^3).
+    auto plane1 = [&](auto edge_tag, int q) {
+      constexpr bool EDGE = decltype(edge_tag)::value;
       const bool has_next = q + 1 <= nx - 1;
       if (has_next) wait_in(q + 1);
       const int t1 = q - qlo;
@@ -171,14 +176,21 @@ __global__ void __launch_bounds__(kTBThreads, 1) k_diffusion_tb2(const TB2Args a
         const float kr = klast ? xc[k].w : rowp[4];    // IMIN(k+1, nz-1)
         const float4 o = cell4(c, xc[k], xn, xp[k], fjp, fjm, kl, kr);
         float* dst = out + k * nz;
-        if (real >> k & 1) *reinterpret_cast<float4*>(dst) = o;
-        if (dup_up >> k & 1) *reinterpret_cast<float4*>(dst - nz) = o;
-        if (dup_dn >> k & 1) *reinterpret_cast<float4*>(dst + nz) = o;
+        if (!EDGE || (real >> k & 1)) *reinterpret_cast<float4*>(dst) = o;
+        if (EDGE && (dup_up >> k & 1)) *reinterpret_cast<float4*>(dst - nz) = o;
+        if (EDGE && (dup_dn >> k & 1)) *reinterpret_cast<float4*>(dst + nz) = o;
         xp[k] = xc[k];
         xc[k] = xn;
       }
       mbar_arrive(full_s1 + t1 % NS1);
       mbar_arrive(empty_in + (q - lo_in) % NST);
+    };
+    // warp-uniform (a warp is one row block): rows outside the grid or edge duplicates
+    const bool edge = real != (1u << S1) - 1 || dup_up || dup_dn;
+    if (edge) {
+      for (int q = qlo; q <= qhi; ++q) plane1(std::true_type{}, q);
+    } else {
+      for (int q = qlo; q <= qhi; ++q) plane1(std::false_type{}, q);
     }
     return;
   }
