@@ -57,6 +57,9 @@ def parse_args():
                     help="N>1 data exchange: fused peer-memory (p2p: halo reads / position publish inside the kernels) or NCCL")
     ap.add_argument("--dist", action="store_true",
                     help="use the multi-GPU drivers (NCCL) even at world size 1 (smoke-tests the N>1 path)")
+    ap.add_argument("--same-device", action="store_true",
+                    help="test only: every rank on cuda:0 (gloo control plane, p2p transport) -- exercises the "
+                         "N>1 bench path on a one-GPU box; the numbers are not a scaling measurement")
     ap.add_argument("--cpu-seconds", type=float, default=8.0, help="target CPU time per baseline sample")
     return ap.parse_args()
 
@@ -248,7 +251,9 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     from paper_2411_18889_b200 import _lib
     from paper_2411_18889_b200.distributed import ShardedLeapfrog, SlabDiffusion
 
-    dev = torch.device("cuda", local_rank)
+    dev = torch.device("cuda", 0 if args.same_device else local_rank)
+    if args.same_device:
+        args.transport = "p2p"  # NCCL refuses two ranks on one GPU
     torch.cuda.set_device(dev)
     lib = b2.load()
     peaks = measured_peaks()
@@ -261,7 +266,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     def max_over_ranks(x: float) -> float:
         if world == 1:
             return x
-        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        t = torch.tensor([x], dtype=torch.float64, device="cpu" if args.same_device else dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
@@ -359,7 +364,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         step(mk())
     torch.cuda.synchronize(dev)
     barrier()
-    clocks = ClockSampler(local_rank).start() if rank == 0 else None
+    clocks = ClockSampler(dev.index).start() if rank == 0 else None
     torch.cuda.synchronize(dev)
     barrier()
     events = []
@@ -693,7 +698,8 @@ def main():
     if world > 1 or args.dist:
         from paper_2411_18889_b200.distributed import init_distributed
 
-        init_distributed("nccl", timeout_s=900.0)  # a lost rank fails the run instead of hanging it
+        # a lost rank fails the run instead of hanging it
+        init_distributed("gloo" if args.same_device else "nccl", timeout_s=900.0)
     out = run_ours(args, rank, world, local_rank)
     if rank == 0:
         print(json.dumps(out), flush=True)

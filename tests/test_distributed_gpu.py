@@ -143,3 +143,24 @@ def test_p2p_fused_allgather_leapfrog_matches_single_device(tmp_path, world):
     z = np.load(out)
     for a, b in (("p", "lp"), ("v", "lv"), ("a", "la"), ("allpos", "lp")):
         assert np.array_equal(z[a].view(np.uint32), z[b].view(np.uint32)), a
+
+
+def test_bench_n_ranks_path_on_one_gpu(tmp_path):
+    """bench.py's N > 1 path end to end (torchrun, i-shards with the fused position publish,
+    i-slabs with peer-memory halos, max-over-ranks timing, one JSON line from rank 0) with two
+    ranks sharing the one GPU (--same-device: gloo control plane). Not a scaling number."""
+    import json
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2", "--master-addr",
+           "127.0.0.1", "--master-port", str(_port()), "bench.py", "--gpus", "2", "--same-device", "--steps", "2",
+           "--warmup", "3", "--particles", "65536", "--grid", "128", "--dsteps", "4"]
+    out = subprocess.run(cmd, cwd=root, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-3000:]
+    line = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert len(line) == 1, out.stdout[-2000:]
+    d = json.loads(line[0])
+    assert d["n_gpus"] == 2 and d["value"] > 0 and "i-shard x2" in d["config"]["parallelism"]
+    assert d["secondary"]["diffusion"]["value"] > 0 and "i-slabs x2" in d["secondary"]["diffusion"]["config"]["workload"]
