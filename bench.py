@@ -53,8 +53,10 @@ def parse_args():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-diffusion", action="store_true")
     ap.add_argument("--no-configs", action="store_true", help="skip the BASELINE parity configs [0] and [1]")
-    ap.add_argument("--transport", choices=["p2p", "nccl"], default="p2p",
-                    help="N>1 data exchange: fused peer-memory (p2p: halo reads / position publish inside the kernels) or NCCL")
+    ap.add_argument("--transport", choices=["auto", "p2p", "nccl"], default="auto",
+                    help="N>1 data exchange: p2p = fused peer memory (position publish inside the update kernel; "
+                         "halo planes read from the neighbour), nccl = collectives. auto: p2p for the n-body "
+                         "position all-gather, nccl for the diffusion halos (no per-step host barrier)")
     ap.add_argument("--dist", action="store_true",
                     help="use the multi-GPU drivers (NCCL) even at world size 1 (smoke-tests the N>1 path)")
     ap.add_argument("--same-device", action="store_true",
@@ -321,7 +323,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         parallelism = "single GPU"
     else:
         plan_lo = rank * (n // world)
-        nb_transport = args.transport
+        nb_transport = "p2p" if args.transport == "auto" else args.transport
         try:
             sim = ShardedLeapfrog(torch.from_numpy(pos_np[plan_lo:plan_lo + n // world]).to(dev),
                                   torch.from_numpy(vel_np[plan_lo:plan_lo + n // world]).to(dev), EPS, DT,
@@ -482,7 +484,7 @@ def run_diffusion(args, rank, world, dev, stream, peaks, barrier, max_over_ranks
         nxl = g // world
         gen = torch.Generator(device=dev).manual_seed(7 + rank)
         f_local = torch.rand((nxl, g, g), generator=gen, dtype=torch.float32, device=dev)
-        transport = args.transport
+        transport = "nccl" if args.transport == "auto" else args.transport
         try:
             sim = SlabDiffusion(f_local, *dargs, transport=transport)
         except Exception as e:  # noqa: BLE001 -- report and fall back to the NCCL transport
