@@ -144,6 +144,24 @@ int b2_diffusion3d_slab(int nx_local, int ny, int nz, float dx, float dy, float 
                         float kappa, const float *f, const float *halo_lo, const float *halo_hi,
                         float *fn, int i_begin, int i_end, void *stream);
 
+/* Fused slab-halo exchange for i-decomposed multi-GPU diffusion.
+ * Computes planes 0 and nx_local-1 of fn (state step+1) from f (state step)
+ * and the neighbours' edge planes, and publishes this rank's new edge planes.
+ * Halos travel through per-rank mailboxes of tagged 16-byte words (one side =
+ * b2_diffusion3d_mailbox_bytes(ny, nz)): in_lo / in_hi are this rank's sides
+ * fed by rank-1 / rank+1 (NULL at a global boundary: clamp), out_lo / out_hi
+ * the neighbours' sides fed by this rank (peer pointers from b2_ipc_import;
+ * NULL: no neighbour). Mailboxes must be zeroed before the first push.
+ * push_only = 1 publishes the edge planes of state `step` (call once per run
+ * before the first step). No host synchronisation: the kernel polls its
+ * mailbox for rows tagged with the expected state. Planes 1..nx_local-2 are a
+ * b2_diffusion3d_slab(..., halo_lo = halo_hi = NULL, 1, nx_local-1) launch. */
+size_t b2_diffusion3d_mailbox_bytes(int ny, int nz);
+int b2_diffusion3d_slab_edges(int nx_local, int ny, int nz, float dx, float dy, float dz, float dt,
+                              float kappa, const float *f, float *fn, const void *in_lo,
+                              const void *in_hi, void *out_lo, void *out_hi, int step,
+                              int push_only, void *stream);
+
 /* nsteps device-resident steps ping-ponging f <-> fn (no host sync).
  * Grids that fit the chip's shared memory (e.g. 128^3) run all steps in one
  * persistent launch with the field resident in shared memory (bricks

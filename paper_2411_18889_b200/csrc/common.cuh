@@ -50,6 +50,23 @@ __device__ __forceinline__ void st_relaxed_b128(uint4* p, uint4 v) {
                "l"(hi)
                : "memory");
 }
+// System-scope twins for words another GPU writes over NVLink (peer mailboxes).
+__device__ __forceinline__ uint4 ld_relaxed_sys_b128(const uint4* p) {
+  unsigned long long lo, hi;
+  asm volatile("{ .reg .b128 t; ld.relaxed.sys.global.b128 t, [%2]; mov.b128 {%0, %1}, t; }"
+               : "=l"(lo), "=l"(hi)
+               : "l"(p)
+               : "memory");
+  return make_uint4(static_cast<unsigned>(lo), static_cast<unsigned>(lo >> 32), static_cast<unsigned>(hi),
+                    static_cast<unsigned>(hi >> 32));
+}
+__device__ __forceinline__ void st_relaxed_sys_b128(uint4* p, uint4 v) {
+  const unsigned long long lo = (static_cast<unsigned long long>(v.y) << 32) | v.x;
+  const unsigned long long hi = (static_cast<unsigned long long>(v.w) << 32) | v.z;
+  asm volatile("{ .reg .b128 t; mov.b128 t, {%1, %2}; st.relaxed.sys.global.b128 [%0], t; }" ::"l"(p), "l"(lo),
+               "l"(hi)
+               : "memory");
+}
 __device__ __forceinline__ unsigned long long globaltimer_ns() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));

@@ -353,15 +353,13 @@ class SlabDiffusion:
     ``transport="nccl"``: the two edge planes go to the neighbours with grouped
     NCCL send/recv on a comm stream while the interior computes.
 
-    ``transport="p2p"`` (fused halo, no collective): every rank maps its
-    neighbours' field buffers into its address space once (CUDA IPC; peer access
-    over NVLink/NVSwitch), and the boundary-plane stencil launches read the halo
-    planes directly from the neighbour's memory. Ordering is stream-side: each
-    rank records an interprocess event after its step; before the next step a
-    rank makes its stream wait on the neighbours' events (their planes are final
-    and they have finished reading ours). A CPU-only barrier on a gloo group
-    ensures those events were recorded before they are waited on; it never
-    synchronises a GPU.
+    ``transport="p2p"`` (fused halo, no collective, no host synchronisation per
+    step): every rank maps its neighbours' halo mailboxes once (CUDA IPC; peer
+    access over NVLink/NVSwitch). Each step is the interior-plane launch plus one
+    edge-plane kernel (b2_diffusion3d_slab_edges) that polls its own mailbox for
+    the neighbours' rows of the current state -- self-validating 16-byte words
+    {3 values, state tag} -- computes the two edge planes and stores its new edge
+    rows straight into the neighbours' mailboxes.
     """
 
     def __init__(self, f_local: torch.Tensor, dx, dy, dz, dt, kappa=1.0, *, group=None, kernels=None,
@@ -393,61 +391,62 @@ class SlabDiffusion:
 
     # ---- p2p transport -------------------------------------------------------
     def _setup_p2p(self) -> None:
+        """Map the neighbours' halo mailboxes (CUDA IPC) and publish the state-0 edge planes.
+
+        Host synchronisation happens here only (and in close / load_state_dict): once every
+        rank has zeroed its mailbox, steps run with no barrier, event or collective -- the
+        edge kernel polls its mailbox for tagged rows and pushes its own rows to the
+        neighbours (b2_diffusion3d_slab_edges)."""
         lib = _lib.load()
         self.ctrl = dist.new_group(backend="gloo") if dist.get_backend(self.group) != "gloo" else self.group
+        ny, nz = self.f.shape[1:]
+        self._side = int(lib.b2_diffusion3d_mailbox_bytes(ny, nz))
+        self.mbox = torch.zeros(2 * self._side, dtype=torch.uint8, device=self.f.device)  # [fed by rank-1 | by rank+1]
         hb = lib.b2_ipc_handle_bytes()
-        bufs = (self.f, self.fn)  # buffer k holds f_s for s % 2 == k on every rank
-        mine = []
-        for t in bufs:
-            h = ctypes.create_string_buffer(hb)
-            off = ctypes.c_size_t(0)
-            _lib.check(lib.b2_ipc_export(t.data_ptr(), h, ctypes.byref(off)), "ipc_export")
-            mine.append((h.raw, off.value))
-        self.event = torch.cuda.Event(enable_timing=False, interprocess=True)
-        self.event.record(torch.cuda.current_stream(self.f.device))
-        info = {"bufs": mine, "nxl": self.f.shape[0], "event": bytes(self.event.ipc_handle())}
+        h = ctypes.create_string_buffer(hb)
+        off = ctypes.c_size_t(0)
+        _lib.check(lib.b2_ipc_export(self.mbox.data_ptr(), h, ctypes.byref(off)), "ipc_export")
         everyone = [None] * self.world
-        dist.all_gather_object(everyone, info, group=self.ctrl)
-        self._peer = {}  # rank -> (nxl, [ptr0, ptr1], [(ptr, off)], event)
+        dist.all_gather_object(everyone, (h.raw, off.value), group=self.ctrl)
+        self._peer = {}  # rank -> (mapped mailbox base, offset)
         err = None
         try:
             for r in (self.rank - 1, self.rank + 1):
                 if 0 <= r < self.world:
-                    ptrs, opened = [], []
-                    for h, off in everyone[r]["bufs"]:
-                        p = ctypes.c_void_p()
-                        _lib.check(lib.b2_ipc_import(ctypes.create_string_buffer(h, len(h)), off, ctypes.byref(p)),
-                                   "ipc_import")
-                        ptrs.append(p.value)
-                        opened.append((p.value, off))
-                    ev = torch.cuda.Event.from_ipc_handle(self.f.device, everyone[r]["event"])
-                    self._peer[r] = (everyone[r]["nxl"], ptrs, opened, ev)
+                    ph, poff = everyone[r]
+                    ptr = ctypes.c_void_p()
+                    _lib.check(lib.b2_ipc_import(ctypes.create_string_buffer(ph, len(ph)), poff, ctypes.byref(ptr)),
+                               "ipc_import")
+                    self._peer[r] = (ptr.value, poff)
         except Exception as e:  # noqa: BLE001 -- agreed on below so that no rank is left in a collective
             err = e
         ok = torch.tensor([0 if err else 1], dtype=torch.int32)
         dist.all_reduce(ok, op=dist.ReduceOp.MIN, group=self.ctrl)
         if not int(ok.item()):
-            for _, _, opened, _ in self._peer.values():
-                for p, off in opened:
-                    lib.b2_ipc_close(p, off)
+            for p, poff in self._peer.values():
+                lib.b2_ipc_close(p, poff)
             self._peer = {}
             raise _lib.SolomonError(f"p2p halo transport unavailable on some rank: {err or 'peer failure'}")
-        torch.cuda.synchronize(self.f.device)  # f_0 complete everywhere before anyone reads it
-        dist.barrier(group=self.ctrl)
+        base = self.mbox.data_ptr()
+        self._in_lo = base if self.has_lo else None
+        self._in_hi = base + self._side if self.has_hi else None
+        self._out_lo = self._peer[self.rank - 1][0] + self._side if self.has_lo else None  # its side fed by rank+1
+        self._out_hi = self._peer[self.rank + 1][0] if self.has_hi else None              # its side fed by rank-1
+        self._publish_edges()
 
-    def _halo_ptrs(self):
-        """Peer addresses of the neighbours' edge planes of f_s (s = steps_done)."""
-        ny, nz = self.f.shape[1:]
-        plane_bytes = ny * nz * self.f.element_size()
-        par = self.steps_done % 2
-        lo = hi = None
-        if self.has_lo:
-            nxl, ptrs, _, _ = self._peer[self.rank - 1]
-            lo = ptrs[par] + (nxl - 1) * plane_bytes
-        if self.has_hi:
-            _, ptrs, _, _ = self._peer[self.rank + 1]
-            hi = ptrs[par]
-        return lo, hi
+    def _edges(self, push_only: bool) -> None:
+        nxl, ny, nz = self.f.shape
+        _lib.check(_lib.load().b2_diffusion3d_slab_edges(
+            nxl, ny, nz, *self.k.args, self.f.data_ptr(), self.fn.data_ptr(), self._in_lo, self._in_hi,
+            self._out_lo, self._out_hi, self.steps_done, int(push_only), _lib.stream_handle(self.f.device)),
+            "diffusion3d_slab_edges")
+
+    def _publish_edges(self) -> None:
+        """(Re)start the exchange at state steps_done: every mailbox zero, then every rank pushes."""
+        self.mbox.zero_()
+        torch.cuda.synchronize(self.f.device)
+        dist.barrier(group=self.ctrl)
+        self._edges(push_only=True)
 
     def close(self) -> None:
         if self.transport != "p2p" or not getattr(self, "_peer", None):
@@ -455,9 +454,8 @@ class SlabDiffusion:
         torch.cuda.synchronize(self.f.device)
         dist.barrier(group=self.ctrl)
         lib = _lib.load()
-        for _, _, opened, _ in self._peer.values():
-            for p, off in opened:
-                lib.b2_ipc_close(p, off)
+        for p, poff in self._peer.values():
+            lib.b2_ipc_close(p, poff)
         self._peer = {}
         dist.barrier(group=self.ctrl)
 
@@ -494,16 +492,9 @@ class SlabDiffusion:
 
     def _step_p2p(self) -> None:
         nxl = self.f.shape[0]
-        stream = torch.cuda.current_stream(self.f.device)
-        dist.barrier(group=self.ctrl)  # host-side: neighbours recorded their previous-step event
-        for _, _, _, ev in self._peer.values():
-            stream.wait_event(ev)
-        lo, hi = self._halo_ptrs()
-        if nxl > 2:
+        if nxl > 2:  # interior planes need no halo
             self.k.slab(self.f, self.fn, None, None, 1, nxl - 1)
-        self.k.slab(self.f, self.fn, lo, hi, 0, 1)
-        self.k.slab(self.f, self.fn, lo, hi, nxl - 1, nxl)
-        self.event.record(stream)
+        self._edges(push_only=False)  # edge planes + halo exchange, synchronised on the device
 
     def step(self, nsteps: int = 1) -> torch.Tensor:
         for _ in range(nsteps):
@@ -516,7 +507,8 @@ class SlabDiffusion:
         return self.f
 
     def launches_per_step(self) -> int:
-        return 3 if self.f.shape[0] > 2 else 2
+        interior = 1 if self.f.shape[0] > 2 else 0
+        return interior + (1 if self.transport == "p2p" else 2)
 
     # ---- checkpoint / resume -----------------------------------
     def state_dict(self) -> dict:
@@ -535,7 +527,8 @@ class SlabDiffusion:
         self.f.copy_(sd["f"])
         self.steps_done = s
         if self.transport == "p2p":
-            self.event.record(torch.cuda.current_stream(self.f.device))  # neighbours wait for the copy
-        elif self.is_cuda:
-            torch.cuda.current_stream(self.f.device).synchronize()
-        dist.barrier(group=self.group)
+            self._publish_edges()  # restart the halo exchange at the loaded state
+        else:
+            if self.is_cuda:
+                torch.cuda.current_stream(self.f.device).synchronize()
+            dist.barrier(group=self.group)
