@@ -55,8 +55,8 @@ def parse_args():
     ap.add_argument("--no-configs", action="store_true", help="skip the BASELINE parity configs [0] and [1]")
     ap.add_argument("--transport", choices=["auto", "p2p", "nccl"], default="auto",
                     help="N>1 data exchange: p2p = fused peer memory (position publish inside the update kernel; "
-                         "halo planes read from the neighbour), nccl = collectives. auto: p2p for the n-body "
-                         "position all-gather, nccl for the diffusion halos (no per-step host barrier)")
+                         "edge-plane kernel pushing halo rows into the neighbours' mailboxes), nccl = collectives. "
+                         "auto: p2p for both (falls back to nccl if peer mapping fails on any rank)")
     ap.add_argument("--dist", action="store_true",
                     help="use the multi-GPU drivers (NCCL) even at world size 1 (smoke-tests the N>1 path)")
     ap.add_argument("--same-device", action="store_true",
@@ -484,7 +484,7 @@ def run_diffusion(args, rank, world, dev, stream, peaks, barrier, max_over_ranks
         nxl = g // world
         gen = torch.Generator(device=dev).manual_seed(7 + rank)
         f_local = torch.rand((nxl, g, g), generator=gen, dtype=torch.float32, device=dev)
-        transport = "nccl" if args.transport == "auto" else args.transport
+        transport = "p2p" if args.transport == "auto" else args.transport
         try:
             sim = SlabDiffusion(f_local, *dargs, transport=transport)
         except Exception as e:  # noqa: BLE001 -- report and fall back to the NCCL transport

@@ -147,8 +147,8 @@ int b2_diffusion3d_slab(int nx_local, int ny, int nz, float dx, float dy, float 
 /* Fused slab-halo exchange for i-decomposed multi-GPU diffusion.
  * Computes planes 0 and nx_local-1 of fn (state step+1) from f (state step)
  * and the neighbours' edge planes, and publishes this rank's new edge planes.
- * Halos travel through per-rank mailboxes of tagged 16-byte words (one side =
- * b2_diffusion3d_mailbox_bytes(ny, nz)): in_lo / in_hi are this rank's sides
+ * Halos travel through per-rank mailboxes of 16-byte words {value, tag, value,
+ * tag} (one side = b2_diffusion3d_mailbox_bytes(ny, nz)): in_lo / in_hi are this rank's sides
  * fed by rank-1 / rank+1 (NULL at a global boundary: clamp), out_lo / out_hi
  * the neighbours' sides fed by this rank (peer pointers from b2_ipc_import;
  * NULL: no neighbour). Mailboxes must be zeroed before the first push.

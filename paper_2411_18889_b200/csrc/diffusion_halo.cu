@@ -6,9 +6,12 @@
 // One kernel per step computes both edge planes of the slab and moves the
 // halo itself, over peer memory with no collective, no event and no host
 // barrier:
-//   * every rank owns a mailbox per side: [2 step parities][ny rows][ceil(nz/3)]
-//     16-byte words {v0, v1, v2, tag}. A .b128 store/load is single-copy atomic,
-//     so a word carries its own readiness: tag = state index + 1;
+//   * every rank owns a mailbox per side: [2 step parities][ny rows][ceil(nz/2)]
+//     16-byte words {v0, tag, v1, tag}, tag = state index + 1. Each 8-byte half
+//     carries its own tag, so a word is ready when both tags match even if the
+//     fabric splits the 16-byte peer store into 8-byte pieces (the only
+//     atomicity relied on across NVLink; NCCL's LL protocol makes the same
+//     assumption). A word carries its own readiness: no flag, no fence;
 //   * the edge kernel polls its own mailbox for the neighbour's plane of
 //     state s (rows of this CTA only), computes its edge rows of state s+1 and
 //     stores them, tagged, straight into the neighbour's mailbox (NVLink /
@@ -47,7 +50,7 @@ struct EdgeArgs {
 __global__ void __launch_bounds__(kEdgeThreads) k_diffusion_slab_edges(const EdgeArgs a) {
   extern __shared__ __align__(16) float sm[];
   const int nz = a.nz, nz4 = nz >> 2, ny = a.ny, nx = a.nx, TJ = a.TJ;
-  const int n3 = (nz + 2) / 3;
+  const int n2 = (nz + 1) / 2;  // words per row: two values each
   const int side = blockIdx.y;  // 0: plane 0 (halo from rank-1), 1: plane nx-1 (halo from rank+1)
   const int p = side ? nx - 1 : 0;
   const size_t plane = static_cast<size_t>(ny) * nz;
@@ -56,14 +59,13 @@ __global__ void __launch_bounds__(kEdgeThreads) k_diffusion_slab_edges(const Edg
   uint4* out = side ? a.out_hi : a.out_lo;
   const int j0 = blockIdx.x * TJ, rows = min(TJ, ny - j0);
   const int tid = threadIdx.x;
-  auto word = [&](int parity, int j, int t) { return (static_cast<size_t>(parity) * ny + j) * n3 + t; };
+  auto word = [&](int parity, int j, int t) { return (static_cast<size_t>(parity) * ny + j) * n2 + t; };
   auto push = [&](const float* rowsrc, size_t rstride, int state) {  // rows j0.. of state `state` -> out
     const unsigned int tag = static_cast<unsigned int>(state + 1);
-    for (int w = tid; w < rows * n3; w += blockDim.x) {
-      const int r = w / n3, t = w - r * n3, k = 3 * t;
+    for (int w = tid; w < rows * n2; w += blockDim.x) {
+      const int r = w / n2, t = w - r * n2, k = 2 * t;
       const float* src = rowsrc + r * rstride + k;
-      const uint4 v = make_uint4(__float_as_uint(src[0]), k + 1 < nz ? __float_as_uint(src[1]) : 0u,
-                                 k + 2 < nz ? __float_as_uint(src[2]) : 0u, tag);
+      const uint4 v = make_uint4(__float_as_uint(src[0]), tag, k + 1 < nz ? __float_as_uint(src[1]) : 0u, tag);
       st_relaxed_sys_b128(out + word(state & 1, j0 + r, t), v);  // peer GPU memory: system scope
     }
   };
@@ -76,19 +78,18 @@ __global__ void __launch_bounds__(kEdgeThreads) k_diffusion_slab_edges(const Edg
   if (in) {
     const unsigned int want = static_cast<unsigned int>(a.step + 1);
     const unsigned long long t0 = globaltimer_ns();
-    for (int w = tid; w < rows * n3; w += blockDim.x) {
-      const int r = w / n3, t = w - r * n3, k = 3 * t;
+    for (int w = tid; w < rows * n2; w += blockDim.x) {
+      const int r = w / n2, t = w - r * n2, k = 2 * t;
       const uint4* src = in + word(a.step & 1, j0 + r, t);
       uint4 v = ld_relaxed_sys_b128(src);  // written by a peer GPU: system scope
-      while (v.w != want) {  // the neighbour's row is not there yet
+      while (v.y != want || v.w != want) {  // the neighbour's row (both halves) is not there yet
         if (globaltimer_ns() - t0 > 4000000000ull) __trap();  // a dead peer fails the step instead of hanging
         __nanosleep(64);
         v = ld_relaxed_sys_b128(src);
       }
       float* d = halo + r * nz + k;
       d[0] = __uint_as_float(v.x);
-      if (k + 1 < nz) d[1] = __uint_as_float(v.y);
-      if (k + 2 < nz) d[2] = __uint_as_float(v.z);
+      if (k + 1 < nz) d[1] = __uint_as_float(v.z);
     }
   }
   __syncthreads();
@@ -120,7 +121,7 @@ extern "C" {
 
 size_t b2_diffusion3d_mailbox_bytes(int ny, int nz) {
   if (ny <= 0 || nz <= 0) return 0;
-  return 2ull * static_cast<size_t>(ny) * ((nz + 2) / 3) * sizeof(uint4);  // one side: 2 parities
+  return 2ull * static_cast<size_t>(ny) * ((nz + 1) / 2) * sizeof(uint4);  // one side: 2 parities
 }
 
 int b2_diffusion3d_slab_edges(int nx_local, int ny, int nz, float dx, float dy, float dz, float dt, float kappa,

@@ -358,7 +358,7 @@ class SlabDiffusion:
     access over NVLink/NVSwitch). Each step is the interior-plane launch plus one
     edge-plane kernel (b2_diffusion3d_slab_edges) that polls its own mailbox for
     the neighbours' rows of the current state -- self-validating 16-byte words
-    {3 values, state tag} -- computes the two edge planes and stores its new edge
+    {value, tag, value, tag} -- computes the two edge planes and stores its new edge
     rows straight into the neighbours' mailboxes.
     """
 
