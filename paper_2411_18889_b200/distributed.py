@@ -189,6 +189,16 @@ class ShardedLeapfrog:
     def pos(self) -> torch.Tensor:
         return self._bufs[self._cur][self.plan.lo:self.plan.hi]  # contiguous view: in-place gather source
 
+    def _agree_planes(self, ny: int, nz: int) -> None:
+        """Every rank must hold [*, ny, nz] planes (a halo is one plane). Checked collectively,
+        so a mismatch raises on every rank instead of deadlocking the first exchange."""
+        dev = self.f.device if dist.get_backend(self.group) == "nccl" else torch.device("cpu")
+        t = torch.tensor([ny, nz, -ny, -nz], dtype=torch.int64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX, group=self.group)
+        hy, hz, ly, lz = (int(v) for v in t.tolist())
+        if (hy, hz, -ly, -lz) != (ny, nz, ny, nz):
+            raise ValueError(f"ranks hold different planes: ny in [{-ly}, {hy}], nz in [{-lz}, {hz}]")
+
     # ---- p2p transport -------------------------------------------------------
     def _setup_p2p(self) -> None:
         lib = _lib.load()
@@ -375,6 +385,7 @@ class SlabDiffusion:
         self.fn = torch.empty_like(self.f)
         self._bufs = (self.f, self.fn)  # state s lives in _bufs[s % 2]
         ny, nz = self.f.shape[1:]
+        self._agree_planes(ny, nz)
         self.has_lo = self.rank > 0
         self.has_hi = self.rank < self.world - 1
         self.is_cuda = self.f.is_cuda
@@ -388,6 +399,16 @@ class SlabDiffusion:
             if not self.is_cuda:
                 raise ValueError("transport='p2p' needs CUDA tensors")
             self._setup_p2p()
+
+    def _agree_planes(self, ny: int, nz: int) -> None:
+        """Every rank must hold [*, ny, nz] planes (a halo is one plane). Checked collectively,
+        so a mismatch raises on every rank instead of deadlocking the first exchange."""
+        dev = self.f.device if dist.get_backend(self.group) == "nccl" else torch.device("cpu")
+        t = torch.tensor([ny, nz, -ny, -nz], dtype=torch.int64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX, group=self.group)
+        hy, hz, ly, lz = (int(v) for v in t.tolist())
+        if (hy, hz, -ly, -lz) != (ny, nz, ny, nz):
+            raise ValueError(f"ranks hold different planes: ny in [{-ly}, {hy}], nz in [{-lz}, {hz}]")
 
     # ---- p2p transport -------------------------------------------------------
     def _setup_p2p(self) -> None:

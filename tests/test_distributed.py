@@ -314,3 +314,30 @@ def test_sharded_drivers_random_cases(tmp_path, world):
     out = tmp_path / "ok.npy"
     mp.spawn(_random_cases_worker, args=(world, _free_port(), str(out)), nprocs=world, join=True)
     assert np.load(out).all()
+
+
+def _mismatch_worker(rank, world, port, out_path):
+    _init(rank, world, port)
+    from paper_2411_18889_b200.distributed import SlabDiffusion
+
+    args = (0.1, 0.12, 0.09, 1e-3, 1.0)
+    f = torch.zeros((3, 5, 8 if rank == 0 else 12))  # rank 1 holds wider planes
+    try:
+        SlabDiffusion(f, *args, kernels=OracleSlabKernels(*args))
+        msg = "no error"
+    except ValueError as e:
+        msg = str(e)
+    parts = [None] * world
+    dist.all_gather_object(parts, msg)
+    if rank == 0:
+        np.save(out_path, np.array(parts))
+    dist.destroy_process_group()
+
+
+def test_slab_diffusion_rejects_mismatched_planes_on_every_rank(tmp_path):
+    """A plane-shape mismatch raises ValueError on all ranks (checked collectively at setup)
+    instead of one rank raising and the others deadlocking in the first halo exchange."""
+    out = tmp_path / "m.npy"
+    mp.spawn(_mismatch_worker, args=(2, _free_port(), str(out)), nprocs=2, join=True)
+    msgs = np.load(out)
+    assert all("different planes" in m for m in msgs), msgs
