@@ -73,6 +73,32 @@ __device__ __forceinline__ float4 cell4(const Coefs& c, float4 fc, float4 fip, f
   return make_float4(lo.x, lo.y, hi.x, hi.y);
 }
 
+// cell4 with the k-direction terms as scalar FMAs on the halves of the packed
+// accumulators (same per-element operation order, so the same bits): the
+// k-neighbour pairs (f.y, f.z), (f.w, kr), (kl, f.x) straddle register pairs and
+// cost MOVs to build for FFMA2.
+__device__ __forceinline__ float4 cell4k(const Coefs& c, float4 fc, float4 fip, float4 fim, float4 fjp, float4 fjm,
+                                         float kl, float kr) {
+  const float2 ce = make_float2(c.ce, c.ce), cc = make_float2(c.cc, c.cc);
+  const float2 cn = make_float2(c.cn, c.cn);
+  float2 lo = __fmul2_rn(ce, make_float2(fip.x, fip.y));
+  float2 hi = __fmul2_rn(ce, make_float2(fip.z, fip.w));
+  lo = __ffma2_rn(cc, make_float2(fc.x, fc.y), lo);
+  hi = __ffma2_rn(cc, make_float2(fc.z, fc.w), hi);
+  lo = __ffma2_rn(ce, make_float2(fim.x, fim.y), lo);
+  hi = __ffma2_rn(ce, make_float2(fim.z, fim.w), hi);
+  lo = __ffma2_rn(cn, make_float2(fjp.x, fjp.y), lo);
+  hi = __ffma2_rn(cn, make_float2(fjp.z, fjp.w), hi);
+  lo = __ffma2_rn(cn, make_float2(fjm.x, fjm.y), lo);
+  hi = __ffma2_rn(cn, make_float2(fjm.z, fjm.w), hi);
+  float4 o;
+  o.x = __fmaf_rn(c.ct, kl, __fmaf_rn(c.ct, fc.y, lo.x));  // f[k+1] then f[k-1]
+  o.y = __fmaf_rn(c.ct, fc.x, __fmaf_rn(c.ct, fc.z, lo.y));
+  o.z = __fmaf_rn(c.ct, fc.y, __fmaf_rn(c.ct, fc.w, hi.x));
+  o.w = __fmaf_rn(c.ct, fc.z, __fmaf_rn(c.ct, kr, hi.y));
+  return o;
+}
+
 // ---- PTX helpers: mbarrier + bulk async copy (sm_90+/sm_100a) -------------
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));

@@ -33,7 +33,7 @@ namespace b2 {
 // Each compute thread owns one float4 column and S consecutive rows, with the
 // i-1 / i values in registers: the in-plane j neighbours are its own registers
 // except at its block ends, so a cell costs one LDS.128 (i+1), two LDS.32 (k+-1)
-// and the 14 packed-FP32 ops. f is read once and f'' written once: 8 B of HBM
+// and the stencil FMAs (cell4k). f is read once and f'' written once: 8 B of HBM
 // per two cell-updates. Arithmetic and clamps as two single steps: bit-identical.
 struct TB2Args {
   const float* f;
@@ -174,7 +174,7 @@ __global__ void __launch_bounds__(kTBThreads, 1) k_diffusion_tb2(const TB2Args a
         const float4 fjm = k > 0 ? xp[k - 1] : *reinterpret_cast<const float4*>(rowp - nz);  // xp[k-1]: old xc[k-1]
         const float kl = kfirst ? xc[k].x : rowp[-1];  // IMAX(k-1, 0)
         const float kr = klast ? xc[k].w : rowp[4];    // IMIN(k+1, nz-1)
-        const float4 o = cell4(c, xc[k], xn, xp[k], fjp, fjm, kl, kr);
+        const float4 o = cell4k(c, xc[k], xn, xp[k], fjp, fjm, kl, kr);
         float* dst = out + k * nz;
         if (!EDGE || (real >> k & 1)) *reinterpret_cast<float4*>(dst) = o;
         if (EDGE && (dup_up >> k & 1)) *reinterpret_cast<float4*>(dst - nz) = o;
@@ -239,7 +239,7 @@ __global__ void __launch_bounds__(kTBThreads, 1) k_diffusion_tb2(const TB2Args a
       const float4 fjm = k > 0 ? ya[k - 1] : *reinterpret_cast<const float4*>(rowp - nz);  // ya[k-1]: old yb[k-1]
       const float kl = kfirst ? yb[k].x : rowp[-1];
       const float kr = klast ? yb[k].w : rowp[4];
-      if (comp >> k & 1) st_stream(reinterpret_cast<float4*>(dst + k * nz), cell4(c, yb[k], yn, ya[k], fjp, fjm, kl, kr));
+      if (comp >> k & 1) st_stream(reinterpret_cast<float4*>(dst + k * nz), cell4k(c, yb[k], yn, ya[k], fjp, fjm, kl, kr));
       ya[k] = yb[k];
       yb[k] = yn;
     }
