@@ -13,4 +13,7 @@ SOLOMON_DIFF_TEMPORAL=1 ncu --set full --clock-control none --import-source on -
 import sys; sys.path.insert(0,'.')
 import torch, paper_2411_18889_b200 as b2
 g=512; sim = b2.Diffusion3D(b2.init_grid(g,g,g), 1/g,1/g,1/g, 0.1/g**2); sim.run(4); torch.cuda.synchronize()" > /dev/null 2>&1
+# the persistent small-problem paths (BASELINE configs[0] / [1])
+ncu --set full --clock-control none --import-source on -k regex:k_leapfrog_small -s 3 -c 1 -o gpurun_out/prof_small_$TAG python scripts/small_configs.py --which 0 --reps 3 > /dev/null 2>&1
+ncu --set full --clock-control none --import-source on -k regex:k_diffusion_resident -s 2 -c 1 -o gpurun_out/prof_res_$TAG python scripts/small_configs.py --which 1 --reps 3 > /dev/null 2>&1
 ls -la gpurun_out

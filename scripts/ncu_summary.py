@@ -21,11 +21,20 @@ KEEP = {
     "k_diffusion_tb2": ["gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
                         "smsp__issue_active.avg.pct_of_peak_sustained_active",
                         "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed"],
+    "k_leapfrog_small": ["sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active",
+                         "sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active",
+                         "smsp__issue_active.avg.pct_of_peak_sustained_active",
+                         "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed"],
+    "k_diffusion_resident": ["smsp__issue_active.avg.pct_of_peak_sustained_active",
+                             "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed",
+                             "lts__throughput.avg.pct_of_peak_sustained_elapsed"],
 }
 NOTES = {
     "k_force_fast": "N=2^20, 64 j-chunks: DRAM traffic is the 1 GiB partial-sum write; FP32-pipe (register-file) bound",
     "k_diffusion_march": "512^3 step under ncu replay (cold L2); algorithmic 1.074 GB (8 B/cell)",
     "k_diffusion_tb2": "512^3, one launch = two steps, under ncu replay; algorithmic 1.074 GB (8 B/cell per launch)",
+    "k_leapfrog_small": "BASELINE configs[0]: N=4096, all 16 KDK steps in one persistent launch (147 CTAs); FP32 pipe ~half busy -- gather and step-to-step exchange latency",
+    "k_diffusion_resident": "BASELINE configs[1]: 128^3 x 100 steps in one persistent launch (shared-memory-resident bricks); latency-bound per-step face exchange",
 }
 
 
