@@ -62,7 +62,9 @@ def test_distributed_drivers_match_single_device(tmp_path):
         assert np.array_equal(z[a].view(np.uint32), z[b].view(np.uint32)), a
 
 
-def _p2p_worker(rank, world, port, shape, steps, out):
+def _p2p_worker(rank, world, port, shape, steps, out, lag=0.0):
+    import time
+
     import torch.distributed as dist
 
     import paper_2411_18889_b200 as b2
@@ -76,7 +78,13 @@ def _p2p_worker(rank, world, port, shape, steps, out):
     lo = sum(counts[:rank])
     args = (0.1, 0.12, 0.09, 1e-3, 1.0)
     sim = SlabDiffusion(f0[lo:lo + counts[rank]].contiguous().cuda(), *args, transport="p2p")
-    sim.step(steps)
+    if lag:  # the last rank enqueues late every step: its neighbour's edge kernel must wait in the GPU
+        for _ in range(steps):
+            if rank == world - 1:
+                time.sleep(lag)
+            sim.step(1)
+    else:
+        sim.step(steps)
     torch.cuda.synchronize()
     parts = [None] * world
     dist.all_gather_object(parts, sim.f.cpu().numpy())
@@ -99,6 +107,18 @@ def test_p2p_fused_halo_slabs_match_full_grid(tmp_path, world, shape, steps):
 
     out = tmp_path / "p2p.npz"
     mp.spawn(_p2p_worker, args=(world, _port(), shape, steps, str(out)), nprocs=world, join=True)
+    z = np.load(out)
+    assert np.array_equal(z["got"].view(np.uint32), z["want"].view(np.uint32))
+
+
+def test_p2p_halo_waits_for_a_late_neighbour(tmp_path):
+    """The halo has no host barrier: when one rank enqueues each step 0.3 s late, its
+    neighbour's edge kernel polls its mailbox until the rows arrive (well inside the 4 s
+    trap) and the result is still bit-identical."""
+    import torch.multiprocessing as mp
+
+    out = tmp_path / "lag.npz"
+    mp.spawn(_p2p_worker, args=(2, _port(), (12, 20, 64), 4, str(out), 0.3), nprocs=2, join=True)
     z = np.load(out)
     assert np.array_equal(z["got"].view(np.uint32), z["want"].view(np.uint32))
 
