@@ -143,13 +143,14 @@ def _omp_env():
     os.environ.setdefault("OMP_PROC_BIND", "close")
 
 
-def cpu_nbody_sample(pos, target_s: float):
-    """Reference fallback build (-Ofast) on a bounded i-sample against all j. Returns (Ginter/s, ni, seconds)."""
+def cpu_nbody_sample(pos, target_s: float, variant: str = "fast"):
+    """Reference fallback build (-Ofast, or the IEEE -O3 build) on a bounded i-sample against all j.
+    Returns (Ginter/s, ni, seconds)."""
     import numpy as np
 
     import oracle
 
-    ref = oracle.Reference("fast")
+    ref = oracle.Reference(variant)
     n = pos.shape[0]
     rng = np.random.default_rng(1234)
     t0 = time.perf_counter()
@@ -165,10 +166,10 @@ def cpu_nbody_sample(pos, target_s: float):
     return ni * n / dt / 1e9, ni, dt
 
 
-def cpu_diffusion_sample(f_host, args, target_s: float):
+def cpu_diffusion_sample(f_host, args, target_s: float, variant: str = "fast"):
     import oracle
 
-    ref = oracle.Reference("fast")
+    ref = oracle.Reference(variant)
     t0 = time.perf_counter()
     a = ref.diffusion3d(f_host, *args)
     dt0 = max(time.perf_counter() - t0, 1e-4)
@@ -452,6 +453,9 @@ def run_ours(args, rank: int, world: int, local_rank: int):
                                       "sample": f"{ni} random i x {n} j (one sampled force evaluation, {dt:.1f} s), "
                                                 f"oracle/_ref libref_fast (reference listing via its fallback "
                                                 f"lowering, g++ -Ofast -fopenmp), {cpu_info()}"}
+            v3, ni3, dt3 = cpu_nbody_sample(pos_np, args.cpu_seconds / 3, "ieee")
+            result["cpu_baseline"]["ieee"] = {"value": v3, "sample": f"{ni3} random i x {n} j ({dt3:.1f} s), "
+                                                                     "oracle/_ref libref_ieee (g++ -O3 -fopenmp)"}
         except FileNotFoundError as e:
             result["cpu_baseline"] = {"value": None, "unavailable": str(e)}
     return result
@@ -547,6 +551,9 @@ def run_diffusion(args, rank, world, dev, stream, peaks, barrier, max_over_ranks
                                        "cores": int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1)),
                                        "kind": "reference",
                                        "sample": f"{steps} steps of {g}^3 ({dt:.1f} s), oracle/_ref libref_fast"}
+                v3, steps3, dt3 = cpu_diffusion_sample(host_f.numpy(), dargs, args.cpu_seconds / 6, "ieee")
+                out["cpu_baseline"]["ieee"] = {"value": v3, "sample": f"{steps3} steps of {g}^3 ({dt3:.1f} s), "
+                                                                      "oracle/_ref libref_ieee (g++ -O3 -fopenmp)"}
             except FileNotFoundError as e:
                 out["cpu_baseline"] = {"value": None, "unavailable": str(e)}
         del host_f, host_fn
