@@ -154,6 +154,8 @@ class ShardedLeapfrog:
     waits on all updates k-1, each of which followed that peer's force k-1.
     """
 
+    _closed = False  # set by close(): stepping afterwards raises
+
     def __init__(self, pos_local: torch.Tensor, vel_local: torch.Tensor, eps: float, dt: float, *, group=None,
                  kernels=None, potential: bool = False, exact: bool = False, transport: str = "nccl"):
         if transport not in ("nccl", "p2p"):
@@ -243,6 +245,8 @@ class ShardedLeapfrog:
             raise _lib.SolomonError(f"p2p position transport unavailable on some rank: {err or 'peer failure'}")
 
     def _peer_ptrs(self, buf: int):
+        if self._closed:
+            raise RuntimeError("ShardedLeapfrog: the p2p transport was closed")
         off = self.plan.lo * 16  # our slice inside each peer's buffer
         arr = (ctypes.c_void_p * max(len(self._peers), 1))(*[p[0][buf] + off for p in self._peers])
         return arr, len(self._peers)
@@ -267,8 +271,9 @@ class ShardedLeapfrog:
             stream.wait_event(ev)
 
     def close(self) -> None:
-        if self.transport != "p2p" or not getattr(self, "_peers", None):
+        if self.transport != "p2p" or self._closed:
             return
+        self._closed = True
         torch.cuda.synchronize(self.pos_all.device)
         dist.barrier(group=self.ctrl)
         lib = _lib.load()
@@ -372,6 +377,8 @@ class SlabDiffusion:
     rows straight into the neighbours' mailboxes.
     """
 
+    _closed = False  # set by close(): stepping afterwards raises
+
     def __init__(self, f_local: torch.Tensor, dx, dy, dz, dt, kappa=1.0, *, group=None, kernels=None,
                  transport: str = "nccl"):
         if f_local.dim() != 3 or f_local.shape[0] < 2:
@@ -456,6 +463,8 @@ class SlabDiffusion:
         self._publish_edges()
 
     def _edges(self, push_only: bool) -> None:
+        if self._closed:
+            raise RuntimeError("SlabDiffusion: the p2p transport was closed")
         nxl, ny, nz = self.f.shape
         _lib.check(_lib.load().b2_diffusion3d_slab_edges(
             nxl, ny, nz, *self.k.args, self.f.data_ptr(), self.fn.data_ptr(), self._in_lo, self._in_hi,
@@ -470,8 +479,9 @@ class SlabDiffusion:
         self._edges(push_only=True)
 
     def close(self) -> None:
-        if self.transport != "p2p" or not getattr(self, "_peer", None):
+        if self.transport != "p2p" or self._closed:
             return
+        self._closed = True
         torch.cuda.synchronize(self.f.device)
         dist.barrier(group=self.ctrl)
         lib = _lib.load()

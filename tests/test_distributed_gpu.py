@@ -89,6 +89,11 @@ def _p2p_worker(rank, world, port, shape, steps, out, lag=0.0):
     parts = [None] * world
     dist.all_gather_object(parts, sim.f.cpu().numpy())
     sim.close()
+    try:  # the peer mappings are gone: stepping must refuse, not touch unmapped memory
+        sim.step(1)
+        raise AssertionError("step after close did not raise")
+    except RuntimeError:
+        pass
     if rank == 0:
         ref = b2.Diffusion3D(f0.cuda(), *args)
         ref.run(steps)
@@ -144,6 +149,11 @@ def _p2p_nbody_worker(rank, world, port, n, steps, out):
     dist.all_gather_object(parts, (sim.pos.cpu().numpy(), sim.vel.cpu().numpy(), sim.acc.cpu().numpy()))
     allpos = sim.pos_all.cpu().numpy()
     sim.close()
+    try:
+        sim.step(1)
+        raise AssertionError("step after close did not raise")
+    except RuntimeError:
+        pass
     if rank == 0:
         lf = b2.Leapfrog(torch.from_numpy(pos).cuda(), torch.from_numpy(vel).cuda(), 2.0 ** -6, 2.0 ** -7)
         lf.step(steps)
