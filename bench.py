@@ -404,6 +404,9 @@ def run_ours(args, rank: int, world: int, local_rank: int):
             "bound": "fp32", "kernel": "k_force_fast", "achieved": achieved_tf, "peak": fp32_peak,
             "unit": "TFLOP/s", "frac": achieved_tf / fp32_peak if fp32_peak > 0 else None,
             "traffic": ncu_traffic("k_force_fast"),
+            "traffic_note": ("DRAM bytes per launch (ncu --set full): almost all of it is the write of the "
+                             "64 j-chunk partial sums (N x 64 x 16 B) that the update kernel reduces in a fixed "
+                             "order; ~0.2 ms of HBM time in a ~400 ms FP32-bound launch"),
             "flop_per_interaction": FLOP_PER_INTERACTION,
             "peak_source": fp32_source,
             "force_ms": force_avg, "allgather_ms": gather_ms,
