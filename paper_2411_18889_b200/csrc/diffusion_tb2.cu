@@ -255,7 +255,8 @@ __global__ void __launch_bounds__(kTBThreads, 1) k_diffusion_tb2(const TB2Args a
 
 static bool tb2_instantiated(int S1, int S2) {
   return (S1 == 2 && (S2 == 1 || S2 == 2)) || (S1 == 3 && (S2 == 2 || S2 == 3)) ||
-         (S1 == 4 && (S2 == 3 || S2 == 4)) || (S1 == 5 && (S2 == 3 || S2 == 4)) || (S1 == 6 && (S2 == 5 || S2 == 6));
+         (S1 == 4 && (S2 == 3 || S2 == 4)) || (S1 == 5 && (S2 == 3 || S2 == 4)) ||
+         (S1 == 6 && (S2 == 4 || S2 == 5 || S2 == 6));
 }
 
 bool plan_tb2(int nx, int ny, int nz, TB2Plan& best) {
@@ -273,21 +274,28 @@ bool plan_tb2(int nx, int ny, int nz, TB2Plan& best) {
     p.TJ = TJ;
     p.S1 = (TJ + 2 + blocks1 - 1) / blocks1;
     p.S2 = (TJ + blocks2 - 1) / blocks2;
-    if (!tb2_instantiated(p.S1, p.S2) || TJ < 5) continue;  // TJ < 5: recomputed halo rows cost more than they save
+    // TJ < 5 recomputes too many halo rows -- except on 1024-float rows, where one float4
+    // column per thread spans the row and TJ = 4 is the tallest tile that fits.
+    if (!tb2_instantiated(p.S1, p.S2) || TJ < (force_tj ? 1 : nz4 >= 256 ? 4 : 5)) continue;
     p.R1 = std::max(blocks1 * p.S1, blocks2 * p.S2 + 2);  // step-1 rows written / read (one past the last)
     p.R = blocks1 * p.S1 + 2;                             // input rows read by step 1
     p.smem = 256 + (static_cast<size_t>(p.nst) * p.R + static_cast<size_t>(p.ns1) * p.R1) * nz * sizeof(float);
     if (p.smem > cap) continue;
     p.n_jtiles = (ny + TJ - 1) / TJ;
-    const int splits = std::max(1, std::min(di.sms / p.n_jtiles, std::max(1, nx / 8)));
-    p.IC = (nx + splits - 1) / splits;
-    p.grid = p.n_jtiles * ((nx + p.IC - 1) / p.IC);
-    const double waves = std::ceil(static_cast<double>(p.grid) / di.sms);
-    const double util = p.grid / (waves * di.sms);
-    const double score = util * TJ / (TJ + 2.0) * static_cast<double>(p.IC) / (p.IC + 2.0);
-    if (score > best_score) {
-      best_score = score;
-      best = p;
+    // i-splits: enough CTAs to fill the SMs, and a split count that avoids a ragged last wave
+    // (each split re-reads 2 planes and recomputes 2 step-1 planes).
+    const int max_splits = std::max(1, std::min(16, nx / 8));
+    for (int splits = 1; splits <= max_splits; ++splits) {
+      TB2Plan q = p;
+      q.IC = (nx + splits - 1) / splits;
+      q.grid = q.n_jtiles * ((nx + q.IC - 1) / q.IC);
+      const double waves = std::ceil(static_cast<double>(q.grid) / di.sms);
+      const double util = q.grid / (waves * di.sms);
+      const double score = util * TJ / (TJ + 2.0) * static_cast<double>(q.IC) / (q.IC + 2.0);
+      if (score > best_score + 1e-9) {
+        best_score = score;
+        best = q;
+      }
     }
   }
   return best_score > 0;
@@ -305,7 +313,7 @@ int launch_tb2(const TB2Plan& p, int nx, int ny, int nz, const Coefs& c, const f
 #define B2_TB2_CASE(A, B) \
   if (p.S1 == A && p.S2 == B) launch_tb2_t<A, B>(p, a, s); else
   B2_TB2_CASE(2, 1) B2_TB2_CASE(2, 2) B2_TB2_CASE(3, 2) B2_TB2_CASE(3, 3) B2_TB2_CASE(4, 3) B2_TB2_CASE(4, 4)
-  B2_TB2_CASE(5, 3) B2_TB2_CASE(5, 4) B2_TB2_CASE(6, 5) B2_TB2_CASE(6, 6) return B2_EINVAL;
+  B2_TB2_CASE(5, 3) B2_TB2_CASE(5, 4) B2_TB2_CASE(6, 4) B2_TB2_CASE(6, 5) B2_TB2_CASE(6, 6) return B2_EINVAL;
 #undef B2_TB2_CASE
   return launch_status();
 }
