@@ -7,6 +7,7 @@
 #include <cmath>
 #include <cstddef>
 #include <cstdint>
+#include <cstdio>
 #include <type_traits>
 
 #include "diffusion_common.cuh"
@@ -285,7 +286,9 @@ bool plan_tb2(int nx, int ny, int nz, TB2Plan& best) {
     // i-splits: enough CTAs to fill the SMs, and a split count that avoids a ragged last wave
     // (each split re-reads 2 planes and recomputes 2 step-1 planes).
     const int max_splits = std::max(1, std::min(16, nx / 8));
+    static const int force_splits = env_int("SOLOMON_DIFF_TB_SPLITS", 0);  // tuning knob
     for (int splits = 1; splits <= max_splits; ++splits) {
+      if (force_splits && splits != force_splits) continue;
       TB2Plan q = p;
       q.IC = (nx + splits - 1) / splits;
       q.grid = q.n_jtiles * ((nx + q.IC - 1) / q.IC);
@@ -298,6 +301,10 @@ bool plan_tb2(int nx, int ny, int nz, TB2Plan& best) {
       }
     }
   }
+  static const bool verbose = env_int("SOLOMON_DIFF_TB_VERBOSE", 0) != 0;
+  if (verbose && best_score > 0)
+    std::fprintf(stderr, "tb2 plan %dx%dx%d: TJ=%d S=%d,%d IC=%d grid=%d smem=%zu score=%.4f\n", nx, ny, nz, best.TJ,
+                 best.S1, best.S2, best.IC, best.grid, best.smem, best_score);
   return best_score > 0;
 }
 
