@@ -191,6 +191,35 @@ def cpu_info() -> str:
     return "unknown"
 
 
+def nbody_sample_parity(pos_np, acc_np, n_sample: int = 512):
+    """Checker (oracle/_ref, the reference listing built -O3): a random i-sample of a full-size
+    force evaluation against all j. SURVEY §8d tolerance for N = 2^20: relL2 <= 1e-4."""
+    import numpy as np
+
+    import oracle
+
+    n = pos_np.shape[0]
+    idx = np.sort(np.random.default_rng(1234).choice(n, n_sample, replace=False))
+    want = oracle.Reference("ieee").calc_acc(np.ascontiguousarray(pos_np[idx]), pos_np, EPS)
+    got = acc_np[idx]
+    rel = float(np.linalg.norm(got[:, :3] - want[:, :3]) / np.linalg.norm(want[:, :3]))
+    return {"relL2_acc": rel, "tolerance": 1e-4, "ok": rel <= 1e-4,
+            "sample": f"{n_sample} random i x {n} j of the e2e drop-in output vs oracle/_ref libref_ieee"}
+
+
+def diffusion_parity(f0, got, steps, dargs):
+    """Checker: `steps` steps of the reference listing (oracle/_ref, -O3 IEEE build) vs the GPU field."""
+    import numpy as np
+
+    import oracle
+
+    ref = oracle.Reference("ieee")
+    want = ref.diffusion3d(f0, *dargs) if steps == 1 else ref.diffusion_run(f0, steps, *dargs)
+    same = bool(np.array_equal(want.view(np.uint32), got.view(np.uint32)))
+    return {"bit_identical": same, "steps": steps, "checker": "oracle/_ref libref_ieee",
+            **({} if same else {"relL2": float(np.linalg.norm(got - want) / np.linalg.norm(want))})}
+
+
 # ---------------------------------------------------------------------------
 # reference arm
 
@@ -427,6 +456,11 @@ def run_ours(args, rank: int, world: int, local_rank: int):
             lib.calc_acc(n, P(hpos.data_ptr()), P(hacc.data_ptr()), n, P(hpos.data_ptr()), EPS)
         t_e2e = (time.perf_counter() - t0) / k_e2e
         _lib.check(lib.b2_last_error(), "calc_acc drop-in")
+        if rank == 0 and not args.no_cpu_baseline:
+            try:
+                result["parity"] = nbody_sample_parity(pos_np, hacc.numpy())
+            except FileNotFoundError as e:
+                result["parity"] = {"unavailable": str(e)}
         result["e2e"] = {"value": interactions / t_e2e / 1e9, "unit": "Ginteractions/s",
                          "h2d_bytes_per_step": 16 * n, "d2h_bytes_per_step": 16 * n,
                          "api": "calc_acc(Ni, ipos, iacc, Nj, jpos, eps) C drop-in, pinned host buffers "
@@ -543,6 +577,11 @@ def run_diffusion(args, rank, world, dev, stream, peaks, barrier, max_over_ranks
         for _ in range(k):
             lib.diffusion3d(g, g, g, *dargs, P(host_f.data_ptr()), P(host_fn.data_ptr()))
         t = (time.perf_counter() - t0) / k
+        if rank == 0 and not args.no_cpu_baseline:
+            try:
+                out["parity"] = diffusion_parity(host_f.numpy(), host_fn.numpy(), 1, dargs)
+            except FileNotFoundError as e:
+                out["parity"] = {"unavailable": str(e)}
         out["e2e"] = {"value": cells / t / 1e9, "unit": "GLUPS", "h2d_bytes_per_step": int(4 * cells),
                       "d2h_bytes_per_step": int(4 * cells),
                       "api": "diffusion3d(nx,...,f,fn) C drop-in, pinned host buffers, synchronous"}
@@ -596,7 +635,14 @@ def run_diffusion_multistep(args, dev, stream, peaks, g, dargs):
     back.copy_(sim2.field, non_blocking=True)
     torch.cuda.synchronize(dev)
     t_e2e = time.perf_counter() - t0
+    parity = None
+    if not args.no_cpu_baseline:
+        try:
+            parity = diffusion_parity(host.numpy(), back.numpy(), steps, dargs)
+        except FileNotFoundError as e:
+            parity = {"unavailable": str(e)}
     return {
+        "parity": parity,
         "metric": "diffusion GLUPS, multi-step device-resident run (effective)", "value": cells * steps / (ms * 1e-3) / 1e9,
         "unit": "GLUPS", "ms_per_step": ms / steps, "steps": steps, "warmup": 4,
         "config": {"workload": f"Diffusion3D.run({steps}) on {g}^3 FP32 (b2_diffusion3d_run: two steps per HBM pass)",
