@@ -191,7 +191,7 @@ def cpu_info() -> str:
     return "unknown"
 
 
-def nbody_sample_parity(pos_np, acc_np, n_sample: int = 512):
+def nbody_sample_parity(pos_np, acc_np, n_sample: int = 512, what: str = "the e2e drop-in output"):
     """Checker (oracle/_ref, the reference listing built -O3): a random i-sample of a full-size
     force evaluation against all j. SURVEY §8d tolerance for N = 2^20: relL2 <= 1e-4."""
     import numpy as np
@@ -204,7 +204,7 @@ def nbody_sample_parity(pos_np, acc_np, n_sample: int = 512):
     got = acc_np[idx]
     rel = float(np.linalg.norm(got[:, :3] - want[:, :3]) / np.linalg.norm(want[:, :3]))
     return {"relL2_acc": rel, "tolerance": 1e-4, "ok": rel <= 1e-4,
-            "sample": f"{n_sample} random i x {n} j of the e2e drop-in output vs oracle/_ref libref_ieee"}
+            "sample": f"{n_sample} random i x {n} j of {what} vs oracle/_ref libref_ieee"}
 
 
 def diffusion_parity(f0, got, steps, dargs):
@@ -468,6 +468,23 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         del hpos, hacc
     else:
         result["e2e"] = None
+        # parity at the sharded size: every rank publishes its positions, rank 0 checks a sample of
+        # a device force evaluation over the gathered pos_all against the reference build
+        sim.gather()
+        torch.cuda.synchronize(dev)
+        barrier()
+        if rank == 0 and not args.no_cpu_baseline:
+            import paper_2411_18889_b200 as b2
+
+            allpos = sim.pos_all.contiguous()
+            out = torch.empty_like(allpos)
+            b2.calc_acc(n, allpos, out, n, allpos, EPS)
+            try:
+                result["parity"] = nbody_sample_parity(allpos.cpu().numpy(), out.cpu().numpy(),
+                                                       what="calc_acc on rank 0 over pos_all after the sharded run")
+            except FileNotFoundError as e:
+                result["parity"] = {"unavailable": str(e)}
+        barrier()
 
     # ---------------- diffusion ----------------
     if not args.no_diffusion:
