@@ -191,11 +191,12 @@ def test_bench_n_ranks_path_on_one_gpu(tmp_path):
            "--warmup", "3", "--particles", "65536", "--grid", "128", "--dsteps", "4"]
     out = subprocess.run(cmd, cwd=root, capture_output=True, text=True, timeout=600)
     assert out.returncode == 0, out.stderr[-3000:]
-    line = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
-    assert len(line) == 1, out.stdout[-2000:]
+    line = [ln for ln in out.stdout.splitlines() if ln.strip()]
+    assert len(line) == 1, out.stdout[-2000:]  # stdout is the JSON line and nothing else
     d = json.loads(line[0])
     assert d["n_gpus"] == 2 and d["value"] > 0 and "i-shard x2" in d["config"]["parallelism"]
     assert d["secondary"]["diffusion"]["value"] > 0 and "i-slabs x2" in d["secondary"]["diffusion"]["config"]["workload"]
+    assert d["parity"]["ok"] and d["secondary"]["diffusion"]["parity"]["bit_identical"]
 
 
 def _p2p_ckpt_worker(rank, world, port, ckpt, out):
