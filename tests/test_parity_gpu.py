@@ -315,7 +315,8 @@ def test_temporal_blocking_kernel_bit_identical(tmp_path):
         "import oracle, paper_2411_18889_b200 as b2\n"
         "args = (0.03, 0.02, 0.025, 2e-5, 1.0)\n"
         "for shape, steps in [((40, 37, 128), 4), ((13, 9, 512), 5), ((256, 64, 512), 6), ((66, 30, 1024), 2),\n"
-        "                     ((300, 70, 256), 3), ((19, 131, 512), 4), ((9, 512, 128), 7), ((64, 5, 512), 2)]:\n"
+        "                     ((300, 70, 256), 3), ((19, 131, 512), 4), ((9, 512, 128), 7), ((64, 5, 512), 2),\n"
+        "                     ((20, 37, 1024), 5), ((33, 4, 1024), 3)]:\n"
         "    f0 = np.random.default_rng(3).random(shape, dtype=np.float32)\n"
         "    want = oracle.Restatement().diffusion_run(f0, steps, *args)\n"
         "    got = b2.Diffusion3D(torch.from_numpy(f0).cuda(), *args).run(steps).cpu().numpy()\n"
