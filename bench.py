@@ -53,6 +53,8 @@ def parse_args():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-diffusion", action="store_true")
     ap.add_argument("--no-configs", action="store_true", help="skip the BASELINE parity configs [0] and [1]")
+    ap.add_argument("--results", default=None,
+                    help="also append the JSON line to this JSON-lines results file (rank 0)")
     ap.add_argument("--transport", choices=["auto", "p2p", "nccl"], default="auto",
                     help="N>1 data exchange: p2p = fused peer memory (position publish inside the update kernel; "
                          "edge-plane kernel pushing halo rows into the neighbours' mailboxes), nccl = collectives. "
@@ -808,6 +810,14 @@ def _claim_stdout():
     return out
 
 
+def _emit(line: dict, json_out, results: str | None) -> None:
+    text = json.dumps(line)
+    print(text, file=json_out, flush=True)
+    if results:
+        with open(results, "a") as fh:
+            fh.write(text + "\n")
+
+
 def main():
     json_out = _claim_stdout()
     args = parse_args()
@@ -819,7 +829,7 @@ def main():
     if args.impl == "reference":
         out = run_reference(args, rank, world)
         if out is not None:
-            print(json.dumps(out), file=json_out, flush=True)
+            _emit(out, json_out, args.results)
         return
     if world > 1 or args.dist:
         from paper_2411_18889_b200.distributed import init_distributed
@@ -828,7 +838,7 @@ def main():
         init_distributed("gloo" if args.same_device else "nccl", timeout_s=900.0)
     out = run_ours(args, rank, world, local_rank)
     if rank == 0:
-        print(json.dumps(out), file=json_out, flush=True)
+        _emit(out, json_out, args.results)
     if world > 1 or args.dist:
         import torch.distributed as dist
 
