@@ -43,6 +43,9 @@ constexpr int kSmallUnroll = B2_SMALL_UNROLL;
 #define B2_SMALL_PAIRS 2
 #endif
 constexpr int kSmallPairs = B2_SMALL_PAIRS;  // packed i-pairs per thread in the force phase
+#ifndef B2_SMALL_RBATCH
+#define B2_SMALL_RBATCH 8  // chunk partials loaded per batch in the in-order reduce
+#endif
 constexpr int kSmallImax = 32;     // i-particles per CTA (at most; a multiple of 4)
 constexpr int kSmallGather = 10;   // positions gathered per thread: n <= 10 * 512
 
@@ -134,7 +137,22 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_leapfrog_small(const Small
     __syncthreads();
     if (tid < I) {  // fixed order c = 0, 1, ..., as k_kdk_update
       float4 s = part[tid];
-      for (int cc = 1; cc < a.nch; ++cc) {
+      int cc = 1;
+#if B2_SMALL_RBATCH > 1
+      for (; cc + B2_SMALL_RBATCH <= a.nch; cc += B2_SMALL_RBATCH) {  // loads in flight together, adds in order
+        float4 q[B2_SMALL_RBATCH];
+#pragma unroll
+        for (int u = 0; u < B2_SMALL_RBATCH; ++u) q[u] = part[(cc + u) * IB + tid];
+#pragma unroll
+        for (int u = 0; u < B2_SMALL_RBATCH; ++u) {
+          s.x = __fadd_rn(s.x, q[u].x);
+          s.y = __fadd_rn(s.y, q[u].y);
+          s.z = __fadd_rn(s.z, q[u].z);
+          s.w = __fadd_rn(s.w, q[u].w);
+        }
+      }
+#endif
+      for (; cc < a.nch; ++cc) {
         const float4 p = part[cc * IB + tid];
         s.x = __fadd_rn(s.x, p.x);
         s.y = __fadd_rn(s.y, p.y);
