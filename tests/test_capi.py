@@ -90,5 +90,15 @@ def test_argument_validation_before_any_device_work(lib):
     assert L.b2_diffusion3d(4, 4, 4, 1.0, 1.0, 1.0, 0.1, 1.0, 16, 16, None) == _lib.B2_EINVAL  # f == fn
     assert L.b2_diffusion3d_slab(4, 4, 4, 1.0, 1.0, 1.0, 0.1, 1.0, 16, None, None, 32, 3, 2, None) == _lib.B2_EINVAL
     assert L.b2_kdk_update(4, None, None, 16, None, 1, 0.0, 0.0, 0.0, 8, None) == _lib.B2_EINVAL
+    # fused slab halo: mailbox sizing and validation (no device work)
+    assert L.b2_diffusion3d_mailbox_bytes(0, 8) == 0
+    assert L.b2_diffusion3d_mailbox_bytes(4, 8) == 2 * 4 * 4 * 16  # 2 parities x ny rows x ceil(nz/2) words
+    edges = lambda nxl, nz, f, fn, mb, step=0: L.b2_diffusion3d_slab_edges(  # noqa: E731
+        nxl, 4, nz, 1.0, 1.0, 1.0, 0.1, 1.0, f, fn, mb, None, None, None, step, 0, None)
+    assert edges(1, 8, 16, 32, None) == _lib.B2_EINVAL        # a slab needs two planes
+    assert edges(4, 6, 16, 32, None) == _lib.B2_EINVAL        # nz % 4
+    assert edges(4, 8, 16, 16, None) == _lib.B2_EINVAL        # f == fn
+    assert edges(4, 8, 16, 32, None, step=-1) == _lib.B2_EINVAL
+    assert edges(4, 8, 16, 32, 40) == _lib.B2_EALIGN          # mailbox words are 16-byte aligned
     assert L.b2_error_string(_lib.B2_EALIGN) == b"pointer not 16-byte aligned"
     assert L.b2_version().startswith(b"solomon_b200")
