@@ -241,6 +241,7 @@ def test_bench_n_ranks_path_on_one_gpu(tmp_path):
     assert d["n_gpus"] == 2 and d["value"] > 0 and "i-shard x2" in d["config"]["parallelism"]
     assert d["secondary"]["diffusion"]["value"] > 0 and "i-slabs x2" in d["secondary"]["diffusion"]["config"]["workload"]
     assert d["parity"]["ok"] and d["secondary"]["diffusion"]["parity"]["bit_identical"]
+    assert d["e2e"]["value"] > 0 and d["e2e"]["h2d_bytes_per_step"] == 16 * 65536
 
 
 def _p2p_ckpt_worker(rank, world, port, ckpt, out):
