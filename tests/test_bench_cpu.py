@@ -50,3 +50,34 @@ def test_clock_sampler_parses_nvidia_smi_csv(tmp_path):
     s.proc = _P()
     rec = s.stop()
     assert rec == {"sm_mhz": 1965.0, "sm_max_mhz": 1965.0, "reasons": ["sw_power_cap"], "samples": 3}
+
+
+def test_parity_checkers_accept_the_reference_and_reject_perturbations():
+    """bench.py's full-size parity helpers (run as checkers outside the timed regions): the
+    reference's own output passes, a perturbed one fails."""
+    import numpy as np
+
+    import oracle
+
+    if not oracle.Reference.available("ieee"):
+        pytest.skip("oracle/_ref not built")
+    sys.path.insert(0, str(ROOT))
+    import bench
+    from paper_2411_18889_b200.nbody import plummer_numpy
+
+    pos, _ = plummer_numpy(2048, 3)
+    acc = oracle.Reference("ieee").calc_acc(pos, pos, bench.EPS)
+    ok = bench.nbody_sample_parity(pos, acc, n_sample=128)
+    assert ok["ok"] and ok["relL2_acc"] == 0.0
+    bad = acc.copy()
+    bad[:, :3] *= 1.001
+    assert not bench.nbody_sample_parity(pos, bad, n_sample=128)["ok"]
+
+    args = (0.03, 0.02, 0.025, 2e-5, 1.0)
+    f0 = np.random.default_rng(1).random((6, 7, 8), dtype=np.float32)
+    want = oracle.Reference("ieee").diffusion_run(f0, 3, *args)
+    assert bench.diffusion_parity(f0, want, 3, args)["bit_identical"]
+    off = want.copy()
+    off[2, 3, 4] = np.nextafter(off[2, 3, 4], np.float32(2))
+    r = bench.diffusion_parity(f0, off, 3, args)
+    assert not r["bit_identical"] and r["relL2"] > 0
