@@ -11,17 +11,19 @@ import pytest
 ROOT = pathlib.Path(__file__).resolve().parents[1]
 
 
-def test_reference_arm_json_line():
+def test_reference_arm_json_line(tmp_path):
     import oracle
 
     if not oracle.Reference.available("fast"):
         pytest.skip("oracle/_ref not built")
+    results = tmp_path / "results.jsonl"
     out = subprocess.run([sys.executable, "bench.py", "--impl", "reference", "--steps", "1", "--warmup", "0",
-                          "--cpu-seconds", "0.3", "--n", "16384", "--grid", "64"],
+                          "--cpu-seconds", "0.3", "--n", "16384", "--grid", "64", "--results", str(results)],
                          cwd=ROOT, capture_output=True, text=True, timeout=300)
     assert out.returncode == 0, out.stderr[-2000:]
     lines = [ln for ln in out.stdout.splitlines() if ln.strip()]
-    assert len(lines) == 1
+    assert len(lines) == 1  # stdout is the JSON line and nothing else
+    assert results.read_text().splitlines() == lines  # --results appends the same line
     d = json.loads(lines[0])
     assert d["impl"] == "reference" and d["unit"] == "Ginteractions/s" and d["value"] > 0
     assert d["cpu_baseline"]["kind"] == "reference" and d["cpu_baseline"]["cores"] >= 1
