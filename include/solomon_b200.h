@@ -162,6 +162,21 @@ int b2_diffusion3d_slab_edges(int nx_local, int ny, int nz, float dx, float dy, 
                               const void *in_hi, void *out_lo, void *out_hi, int step,
                               int push_only, void *stream);
 
+/* Two-plane halo exchange for two steps per exchange (SlabDiffusion.run,
+ * DESIGN.md §6). f is this rank's halo-extended slab of nx_ext = lo_h +
+ * nx_local + hi_h planes (lo_h / hi_h = 2 with a neighbour on that side, 0 at
+ * a global end). phase 0 pushes this rank's two edge planes of the current
+ * state into the neighbours' mailboxes (out_lo / out_hi: peer pointers from
+ * b2_ipc_import, b2_diffusion3d_mailbox2_bytes(ny, nz) bytes per side);
+ * phase 1 waits in the GPU for the neighbours' planes in this rank's own
+ * mailbox (in_lo / in_hi) and writes them into the halo planes. xchg counts
+ * exchanges from 0 (mailboxes zeroed once before the first). Launch phase 0
+ * then phase 1 on the same stream. */
+size_t b2_diffusion3d_mailbox2_bytes(int ny, int nz);
+int b2_diffusion3d_slab_halo2(int nx_ext, int ny, int nz, int lo_h, int nx_local, float *f,
+                              const void *in_lo, const void *in_hi, void *out_lo, void *out_hi,
+                              int xchg, int phase, void *stream);
+
 /* nsteps device-resident steps ping-ponging f <-> fn (no host sync).
  * Grids that fit the chip's shared memory (e.g. 128^3) run all steps in one
  * persistent launch with the field resident in shared memory (bricks

@@ -50,6 +50,8 @@ SIGNATURES = {
     "b2_diffusion3d_run": (_i, [_i, _i, _i, _f, _f, _f, _f, _f, _p, _p, _i, ctypes.POINTER(_i), _p]),
     "b2_diffusion3d_mailbox_bytes": (_sz, [_i, _i]),
     "b2_diffusion3d_slab_edges": (_i, [_i, _i, _i, _f, _f, _f, _f, _f, _p, _p, _p, _p, _p, _p, _i, _i, _p]),
+    "b2_diffusion3d_mailbox2_bytes": (_sz, [_i, _i]),
+    "b2_diffusion3d_slab_halo2": (_i, [_i, _i, _i, _i, _i, _p, _p, _p, _p, _p, _i, _i, _p]),
     "b2_ipc_handle_bytes": (_sz, []),
     "b2_ipc_export": (_i, [_p, _p, ctypes.POINTER(_sz)]),
     "b2_ipc_import": (_i, [_p, _sz, ctypes.POINTER(_p)]),

@@ -113,6 +113,67 @@ __global__ void __launch_bounds__(kEdgeThreads) k_diffusion_slab_edges(const Edg
   if (out) push(res, nz, a.step + 1);
 }
 
+// ---------------------------------------------------------------------------
+// Two-plane halo exchange for SlabDiffusion.run (two steps per exchange):
+// between two-step passes each rank ships its two edge planes of the current state to
+// each neighbour and takes the neighbours' into the halo planes of its halo-extended
+// slab [lo_h halo | nx_local own | hi_h halo] (lo_h, hi_h = 2, or 0 at a global end,
+// where the pass's own clamp applies). Same self-validating words as above, one
+// 8-byte half per value pair: {v, tag, v, tag}, tag = exchange index + 1, two
+// exchange parities. Phase 0 pushes (no waiting); phase 1 polls its own mailbox and
+// writes the halo planes. Two launches, so every push of a rank is issued before any
+// of its CTAs waits: no cross-rank cycle whatever the residency.
+struct Xchg2Args {
+  float* f;
+  int ny, nz, TJ;
+  int lo_h, nxl;
+  const uint4* in_lo;  // my mailbox sides, fed by rank-1 / rank+1 (null: global end)
+  const uint4* in_hi;
+  uint4* out_lo;  // the neighbours' sides fed by me (null: no neighbour)
+  uint4* out_hi;
+  int xchg, phase;
+};
+
+__global__ void __launch_bounds__(kEdgeThreads) k_diffusion_slab_halo2(const Xchg2Args a) {
+  const int ny = a.ny, nz = a.nz, n2 = (nz + 1) / 2;
+  const int side = blockIdx.y;
+  const int j0 = blockIdx.x * a.TJ, rows = min(a.TJ, ny - j0);
+  const size_t plane = static_cast<size_t>(ny) * nz;
+  const int parity = a.xchg & 1;
+  const unsigned int tag = static_cast<unsigned int>(a.xchg + 1);
+  auto word = [&](int p, int j, int t) { return ((static_cast<size_t>(parity) * 2 + p) * ny + j) * n2 + t; };
+  const int per_plane = rows * n2;
+  if (a.phase == 0) {
+    uint4* out = side ? a.out_hi : a.out_lo;
+    if (!out) return;
+    const int first = side ? a.lo_h + a.nxl - 2 : a.lo_h;  // my two planes next to that neighbour
+    for (int w = threadIdx.x; w < 2 * per_plane; w += blockDim.x) {
+      const int p = w / per_plane, rem = w - p * per_plane, r = rem / n2, t = rem - r * n2, k = 2 * t;
+      const float* src = a.f + static_cast<size_t>(first + p) * plane + static_cast<size_t>(j0 + r) * nz + k;
+      st_relaxed_sys_b128(out + word(p, j0 + r, t),
+                          make_uint4(__float_as_uint(src[0]), tag, k + 1 < nz ? __float_as_uint(src[1]) : 0u, tag));
+    }
+    return;
+  }
+  const uint4* in = side ? a.in_hi : a.in_lo;
+  if (!in) return;
+  const int dst0 = side ? a.lo_h + a.nxl : 0;  // my halo planes on that side
+  const unsigned long long t0 = globaltimer_ns();
+  for (int w = threadIdx.x; w < 2 * per_plane; w += blockDim.x) {
+    const int p = w / per_plane, rem = w - p * per_plane, r = rem / n2, t = rem - r * n2, k = 2 * t;
+    const uint4* src = in + word(p, j0 + r, t);
+    uint4 v = ld_relaxed_sys_b128(src);
+    while (v.y != tag || v.w != tag) {
+      if (globaltimer_ns() - t0 > 4000000000ull) __trap();  // a dead peer fails the run instead of hanging
+      __nanosleep(64);
+      v = ld_relaxed_sys_b128(src);
+    }
+    float* d = a.f + static_cast<size_t>(dst0 + p) * plane + static_cast<size_t>(j0 + r) * nz + k;
+    d[0] = __uint_as_float(v.x);
+    if (k + 1 < nz) d[1] = __uint_as_float(v.z);
+  }
+}
+
 }  // namespace b2
 
 using namespace b2;
@@ -151,6 +212,36 @@ int b2_diffusion3d_slab_edges(int nx_local, int ny, int nz, float dx, float dy, 
              make_coefs(dx, dy, dz, dt, kappa)};
   const dim3 grid((ny + TJ - 1) / TJ, 2);
   k_diffusion_slab_edges<<<grid, kEdgeThreads, push_only ? 0 : smem, as_stream(stream)>>>(a);
+  return launch_status();
+}
+
+size_t b2_diffusion3d_mailbox2_bytes(int ny, int nz) {
+  if (ny <= 0 || nz <= 0) return 0;
+  return 4ull * static_cast<size_t>(ny) * ((nz + 1) / 2) * sizeof(uint4);  // one side: 2 parities x 2 planes
+}
+
+int b2_diffusion3d_slab_halo2(int nx_ext, int ny, int nz, int lo_h, int nx_local, float* f, const void* in_lo,
+                              const void* in_hi, void* out_lo, void* out_hi, int xchg, int phase, void* stream) {
+  const int hi_h = nx_ext - lo_h - nx_local;
+  if (nx_local < 2 || ny <= 0 || nz <= 0 || !f || xchg < 0 || (phase != 0 && phase != 1) ||
+      (lo_h != 0 && lo_h != 2) || (hi_h != 0 && hi_h != 2) || (in_lo && lo_h != 2) || (in_hi && hi_h != 2))
+    return B2_EINVAL;
+  if (!aligned16(in_lo) || !aligned16(in_hi) || !aligned16(out_lo) || !aligned16(out_hi)) return B2_EALIGN;
+  const int n2 = (nz + 1) / 2;
+  const int TJ = std::max(1, std::min(ny, 2048 / (2 * n2)));
+  Xchg2Args a{f,
+              ny,
+              nz,
+              TJ,
+              lo_h,
+              nx_local,
+              static_cast<const uint4*>(in_lo),
+              static_cast<const uint4*>(in_hi),
+              static_cast<uint4*>(out_lo),
+              static_cast<uint4*>(out_hi),
+              xchg,
+              phase};
+  k_diffusion_slab_halo2<<<dim3((ny + TJ - 1) / TJ, 2), kEdgeThreads, 0, as_stream(stream)>>>(a);
   return launch_status();
 }
 

@@ -74,6 +74,15 @@ class CudaSlabKernels:
                    "diffusion3d_slab")
 
 
+    def run2(self, f, fn) -> bool:
+        """Two steps over a (halo-extended) slab; True when the result is in fn."""
+        nx, ny, nz = f.shape
+        in_fn = ctypes.c_int(0)
+        _lib.check(self.lib.b2_diffusion3d_run(nx, ny, nz, *self.args, f.data_ptr(), fn.data_ptr(), 2,
+                                               ctypes.byref(in_fn), _lib.stream_handle(f.device)), "diffusion3d_run")
+        return bool(in_fn.value)
+
+
 def _all_gather_inplace(out: torch.Tensor, local: torch.Tensor, group=None) -> None:
     if dist.get_backend(group) == "nccl":
         dist.all_gather_into_tensor(out, local, group=group)
@@ -429,7 +438,9 @@ class SlabDiffusion:
         self.ctrl = dist.new_group(backend="gloo") if dist.get_backend(self.group) != "gloo" else self.group
         ny, nz = self.f.shape[1:]
         self._side = int(lib.b2_diffusion3d_mailbox_bytes(ny, nz))
-        self.mbox = torch.zeros(2 * self._side, dtype=torch.uint8, device=self.f.device)  # [fed by rank-1 | by rank+1]
+        self._side2 = int(lib.b2_diffusion3d_mailbox2_bytes(ny, nz))
+        # [per-step: fed by rank-1 | by rank+1][run(): fed by rank-1 | by rank+1]
+        self.mbox = torch.zeros(2 * self._side + 2 * self._side2, dtype=torch.uint8, device=self.f.device)
         hb = lib.b2_ipc_handle_bytes()
         h = ctypes.create_string_buffer(hb)
         off = ctypes.c_size_t(0)
@@ -460,6 +471,10 @@ class SlabDiffusion:
         self._in_hi = base + self._side if self.has_hi else None
         self._out_lo = self._peer[self.rank - 1][0] + self._side if self.has_lo else None  # its side fed by rank+1
         self._out_hi = self._peer[self.rank + 1][0] if self.has_hi else None              # its side fed by rank-1
+        r2 = 2 * self._side  # run() mailboxes, same layout after the per-step pair
+        self._in2 = (base + r2 if self.has_lo else None, base + r2 + self._side2 if self.has_hi else None)
+        self._out2 = (self._peer[self.rank - 1][0] + r2 + self._side2 if self.has_lo else None,
+                      self._peer[self.rank + 1][0] + r2 if self.has_hi else None)
         self._publish_edges()
 
     def _edges(self, push_only: bool) -> None:
@@ -472,8 +487,9 @@ class SlabDiffusion:
             "diffusion3d_slab_edges")
 
     def _publish_edges(self) -> None:
-        """(Re)start the exchange at state steps_done: every mailbox zero, then every rank pushes."""
-        self.mbox.zero_()
+        """(Re)start the per-step exchange at state steps_done: every per-step mailbox zero, then
+        every rank pushes. (run()'s mailboxes keep their monotonic exchange tags.)"""
+        self.mbox[:2 * self._side].zero_()
         torch.cuda.synchronize(self.f.device)
         dist.barrier(group=self.ctrl)
         self._edges(push_only=True)
@@ -536,6 +552,68 @@ class SlabDiffusion:
             self.f, self.fn = self.fn, self.f
             self.steps_done += 1
         return self.f
+
+    # ---- two steps per exchange ------------------------------------------------
+    def run(self, nsteps: int) -> torch.Tensor:
+        """Advance ``nsteps`` with TWO steps per halo exchange (collective, bit-identical to
+        ``step(nsteps)``). Each rank keeps a halo-extended copy of its slab with two neighbour
+        planes per side; a pass is one ``b2_diffusion3d_run(..., 2)`` over it (on large slabs
+        the two-steps-per-HBM-pass kernel), the two planes next to the halo are exact after
+        two steps and the two halo planes are refreshed between passes (NCCL send/recv, or
+        over peer memory with ``b2_diffusion3d_slab_halo2`` for transport="p2p"). An odd
+        remainder step runs through ``step(1)``."""
+        if nsteps < 0:
+            raise ValueError("nsteps must be >= 0")
+        pairs = nsteps // 2
+        if pairs:
+            nxl = self.f.shape[0]
+            lo_h = 2 if self.has_lo else 0
+            cur, oth = self._ext_buffers(lo_h + nxl + (2 if self.has_hi else 0))
+            cur[lo_h:lo_h + nxl].copy_(self.f)
+            for _ in range(pairs):
+                self._halo2(cur, lo_h, nxl)
+                if self.k.run2(cur, oth):
+                    cur, oth = oth, cur
+            self.f.copy_(cur[lo_h:lo_h + nxl])
+            self.steps_done += 2 * pairs
+            if self.transport == "p2p":
+                self._publish_edges()  # the per-step halo restarts at the new state
+        if nsteps % 2:
+            self.step(1)
+        return self.f
+
+    def _ext_buffers(self, nx_ext: int):
+        ext = getattr(self, "_ext", None)
+        if ext is None or ext[0].shape[0] != nx_ext:
+            shape = (nx_ext,) + tuple(self.f.shape[1:])
+            ext = (torch.zeros(shape, dtype=self.f.dtype, device=self.f.device),
+                   torch.zeros(shape, dtype=self.f.dtype, device=self.f.device))
+            self._ext = ext
+        return ext
+
+    def _halo2(self, cur: torch.Tensor, lo_h: int, nxl: int) -> None:
+        """Fill cur's halo planes with the neighbours' two edge planes of the same state."""
+        if self.transport == "p2p":
+            if self._closed:
+                raise RuntimeError("SlabDiffusion: the p2p transport was closed")
+            nx_ext, ny, nz = cur.shape
+            xchg = getattr(self, "_xchg", 0)
+            lib, sh = _lib.load(), _lib.stream_handle(cur.device)
+            for phase in (0, 1):  # push everything, then wait for the neighbours' planes
+                _lib.check(lib.b2_diffusion3d_slab_halo2(nx_ext, ny, nz, lo_h, nxl, cur.data_ptr(), *self._in2,
+                                                         *self._out2, xchg, phase, sh), "diffusion3d_slab_halo2")
+            self._xchg = xchg + 1
+            return
+        ops, g = [], self.group
+        if self.has_lo:
+            ops.append(dist.P2POp(dist.isend, cur[lo_h:lo_h + 2], self.rank - 1, g))
+            ops.append(dist.P2POp(dist.irecv, cur[0:2], self.rank - 1, g))
+        if self.has_hi:
+            ops.append(dist.P2POp(dist.isend, cur[lo_h + nxl - 2:lo_h + nxl], self.rank + 1, g))
+            ops.append(dist.P2POp(dist.irecv, cur[lo_h + nxl:lo_h + nxl + 2], self.rank + 1, g))
+        if ops:
+            for r in dist.batch_isend_irecv(ops):
+                r.wait()
 
     def launches_per_step(self) -> int:
         interior = 1 if self.f.shape[0] > 2 else 0

@@ -46,6 +46,10 @@ class OracleSlabKernels:
         self.o = oracle.Restatement()
         self.args = args
 
+    def run2(self, f, fn):
+        fn.numpy()[...] = self.o.diffusion_run(f.numpy(), 2, *self.args)
+        return True
+
     def slab(self, f, fn, halo_lo, halo_hi, i_begin, i_end):
         a = f.numpy()
         lo = halo_lo.numpy() if halo_lo is not None else a[0]  # absent halo == clamp IMAX(i-1,0)
@@ -341,3 +345,36 @@ def test_slab_diffusion_rejects_mismatched_planes_on_every_rank(tmp_path):
     mp.spawn(_mismatch_worker, args=(2, _free_port(), str(out)), nprocs=2, join=True)
     msgs = np.load(out)
     assert all("different planes" in m for m in msgs), msgs
+
+
+def _run2_worker(rank, world, port, counts, ny, nz, steps, out_path):
+    _init(rank, world, port)
+    from paper_2411_18889_b200.distributed import SlabDiffusion
+
+    f0 = np.random.default_rng(6).random((sum(counts), ny, nz), dtype=np.float32)
+    args = (0.1, 0.12, 0.09, 1e-3, 1.0)
+    lo = sum(counts[:rank])
+    sim = SlabDiffusion(torch.from_numpy(f0[lo:lo + counts[rank]].copy()), *args, kernels=OracleSlabKernels(*args))
+    sim.run(steps[0])
+    sim.step(1)          # the per-step path continues from run()'s state
+    sim.run(steps[1])
+    parts = [None] * world
+    dist.all_gather_object(parts, (sim.f.numpy(), sim.steps_done))
+    if rank == 0:
+        np.save(out_path, np.concatenate([p[0] for p in parts], axis=0))
+        assert all(p[1] == steps[0] + 1 + steps[1] for p in parts)
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,counts,steps", [(2, (3, 4), (4, 5)), (3, (2, 5, 3), (6, 2)), (4, (2, 2, 3, 2), (3, 4))])
+def test_slab_run_two_steps_per_exchange_equals_full_grid(tmp_path, world, counts, steps):
+    """SlabDiffusion.run: two steps per exchange of two halo planes (uneven slabs, odd
+    remainders, mixed with step()) == the full-grid oracle run, bit for bit."""
+    import oracle
+
+    out = tmp_path / "r.npy"
+    ny, nz = 5, 7
+    mp.spawn(_run2_worker, args=(world, _free_port(), counts, ny, nz, steps, str(out)), nprocs=world, join=True)
+    f0 = np.random.default_rng(6).random((sum(counts), ny, nz), dtype=np.float32)
+    want = oracle.Restatement().diffusion_run(f0, steps[0] + 1 + steps[1], 0.1, 0.12, 0.09, 1e-3, 1.0)
+    assert np.array_equal(np.load(out).view(np.uint32), want.view(np.uint32))

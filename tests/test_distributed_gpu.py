@@ -43,8 +43,9 @@ def _worker(rank, port, out):
     f = b2.init_grid(16, 24, 32, seed=2)
     sd = SlabDiffusion(f, 0.1, 0.1, 0.1, 1e-3, 1.0)
     sd.step(3)
+    sd.run(5)  # two steps per exchange (world 1: the pass alone)
     ref = b2.Diffusion3D(f.clone(), 0.1, 0.1, 0.1, 1e-3, 1.0)
-    ref.run(3)
+    ref.run(8)
     torch.cuda.synchronize()
     np.savez(out, sp=sh.pos.cpu().numpy(), sv=sh.vel.cpu().numpy(), sa=sh.acc.cpu().numpy(),
              lp=lf.pos.cpu().numpy(), lv=lf.vel.cpu().numpy(), la=lf.acc.cpu().numpy(),
@@ -170,6 +171,45 @@ def test_p2p_halo_random_slabs(tmp_path):
     out = tmp_path / "rand.npy"
     mp.spawn(_p2p_random_worker, args=(3, _port(), str(out)), nprocs=3, join=True)
     assert np.load(out).all()
+
+
+def _p2p_run_worker(rank, world, port, counts, ny, nz, steps, out):
+    import torch.distributed as dist
+
+    import paper_2411_18889_b200 as b2
+    from paper_2411_18889_b200.distributed import SlabDiffusion
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    f0 = np.random.default_rng(12).random((sum(counts), ny, nz), dtype=np.float32)
+    args = (0.03, 0.025, 0.02, 2e-5, 1.0)
+    lo = sum(counts[:rank])
+    sim = SlabDiffusion(torch.from_numpy(f0[lo:lo + counts[rank]]).cuda(), *args, transport="p2p")
+    sim.run(steps[0])
+    sim.step(1)  # the per-step fused halo resumes from run()'s state
+    sim.run(steps[1])
+    torch.cuda.synchronize()
+    parts = [None] * world
+    dist.all_gather_object(parts, sim.f.cpu().numpy())
+    sim.close()
+    if rank == 0:
+        want = b2.Diffusion3D(torch.from_numpy(f0).cuda(), *args).run(steps[0] + 1 + steps[1]).cpu().numpy()
+        np.savez(out, got=np.concatenate(parts, axis=0), want=want)
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,counts,ny,nz,steps", [(2, (3, 5), 20, 64, (4, 3)), (3, (2, 4, 3), 9, 1024, (6, 2)),
+                                                      (4, (9, 7, 8, 8), 40, 128, (5, 6))])
+def test_p2p_run_two_steps_per_exchange(tmp_path, world, counts, ny, nz, steps):
+    """SlabDiffusion.run over the p2p transport: two-plane halos through peer-memory mailboxes
+    (b2_diffusion3d_slab_halo2) every two steps, mixed with step(); bit-identical."""
+    import torch.multiprocessing as mp
+
+    out = tmp_path / "run2.npz"
+    mp.spawn(_p2p_run_worker, args=(world, _port(), counts, ny, nz, steps, str(out)), nprocs=world, join=True)
+    z = np.load(out)
+    assert np.array_equal(z["got"].view(np.uint32), z["want"].view(np.uint32))
 
 
 def _p2p_nbody_worker(rank, world, port, n, steps, out):
