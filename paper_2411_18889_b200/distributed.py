@@ -397,13 +397,18 @@ class SlabDiffusion:
         self.group = group
         self.world, self.rank = dist.get_world_size(group), dist.get_rank(group)
         self.k = kernels or CudaSlabKernels(dx, dy, dz, dt, kappa)
-        self.f = f_local.contiguous().clone()
-        self.fn = torch.empty_like(self.f)
-        self._bufs = (self.f, self.fn)  # state s lives in _bufs[s % 2]
-        ny, nz = self.f.shape[1:]
-        self._agree_planes(ny, nz)
+        nxl, ny, nz = f_local.shape
         self.has_lo = self.rank > 0
         self.has_hi = self.rank < self.world - 1
+        # f / fn are views of two halo-extended slabs [2 halo | nx_local | 2 halo] (no halo at a
+        # global end): step() works on the views, run() on the whole slabs without copies
+        self._lo_h = 2 if self.has_lo else 0
+        ext = (self._lo_h + nxl + (2 if self.has_hi else 0), ny, nz)
+        self._ext = (torch.zeros(ext, dtype=f_local.dtype, device=f_local.device),
+                     torch.zeros(ext, dtype=f_local.dtype, device=f_local.device))
+        self.f, self.fn = (e[self._lo_h:self._lo_h + nxl] for e in self._ext)
+        self.f.copy_(f_local)
+        self._agree_planes(ny, nz)
         self.is_cuda = self.f.is_cuda
         self.transport = transport
         self.steps_done = 0
@@ -566,30 +571,19 @@ class SlabDiffusion:
             raise ValueError("nsteps must be >= 0")
         pairs = nsteps // 2
         if pairs:
-            nxl = self.f.shape[0]
-            lo_h = 2 if self.has_lo else 0
-            cur, oth = self._ext_buffers(lo_h + nxl + (2 if self.has_hi else 0))
-            cur[lo_h:lo_h + nxl].copy_(self.f)
+            nxl, lo_h = self.f.shape[0], self._lo_h
+            cur, oth = self._ext if self.f.data_ptr() == self._ext[0][lo_h].data_ptr() else self._ext[::-1]
             for _ in range(pairs):
                 self._halo2(cur, lo_h, nxl)
                 if self.k.run2(cur, oth):
                     cur, oth = oth, cur
-            self.f.copy_(cur[lo_h:lo_h + nxl])
+            self.f, self.fn = cur[lo_h:lo_h + nxl], oth[lo_h:lo_h + nxl]
             self.steps_done += 2 * pairs
             if self.transport == "p2p":
                 self._publish_edges()  # the per-step halo restarts at the new state
         if nsteps % 2:
             self.step(1)
         return self.f
-
-    def _ext_buffers(self, nx_ext: int):
-        ext = getattr(self, "_ext", None)
-        if ext is None or ext[0].shape[0] != nx_ext:
-            shape = (nx_ext,) + tuple(self.f.shape[1:])
-            ext = (torch.zeros(shape, dtype=self.f.dtype, device=self.f.device),
-                   torch.zeros(shape, dtype=self.f.dtype, device=self.f.device))
-            self._ext = ext
-        return ext
 
     def _halo2(self, cur: torch.Tensor, lo_h: int, nxl: int) -> None:
         """Fill cur's halo planes with the neighbours' two edge planes of the same state."""
@@ -625,14 +619,13 @@ class SlabDiffusion:
                 "steps": self.steps_done}
 
     def load_state_dict(self, sd: dict) -> None:
-        """Collective: every rank loads its own slab. The field goes into the buffer
-        that holds state ``steps`` (the p2p transport addresses peers by that parity)."""
+        """Collective: every rank loads its own slab; the halo exchange restarts at the
+        loaded state."""
         if sd.get("kind") != "SlabDiffusion":
             raise ValueError(f"not a SlabDiffusion checkpoint: {sd.get('kind')!r}")
         if (sd["world"], sd["rank"]) != (self.world, self.rank) or tuple(sd["f"].shape) != tuple(self.f.shape):
             raise ValueError("checkpoint is for a different decomposition")
         s = int(sd["steps"])
-        self.f, self.fn = self._bufs[s % 2], self._bufs[1 - s % 2]
         self.f.copy_(sd["f"])
         self.steps_done = s
         if self.transport == "p2p":

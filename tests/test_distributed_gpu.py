@@ -282,6 +282,8 @@ def test_bench_n_ranks_path_on_one_gpu(tmp_path):
     assert d["secondary"]["diffusion"]["value"] > 0 and "i-slabs x2" in d["secondary"]["diffusion"]["config"]["workload"]
     assert d["parity"]["ok"] and d["secondary"]["diffusion"]["parity"]["bit_identical"]
     assert d["e2e"]["value"] > 0 and d["e2e"]["h2d_bytes_per_step"] == 16 * 65536
+    run = d["secondary"]["diffusion"]["run"]
+    assert run["value"] > 0 and run["parity"]["bit_identical"]
 
 
 def _p2p_ckpt_worker(rank, world, port, ckpt, out):
