@@ -1,6 +1,6 @@
-"""compute-sanitizer workload for the fused slab halo (k_diffusion_slab_edges): two ranks share
-cuda:0 (gloo control plane, CUDA IPC mailboxes), a few p2p SlabDiffusion steps, checked against
-the single-device run. Run as
+"""compute-sanitizer workload for the fused slab halos (k_diffusion_slab_edges and
+k_diffusion_slab_halo2): two ranks share cuda:0 (gloo control plane, CUDA IPC mailboxes),
+p2p SlabDiffusion step() and run(), checked against the single-device run. Run as
     compute-sanitizer --tool memcheck --target-processes all python scripts/sanitize_halo.py
 """
 from __future__ import annotations
@@ -30,12 +30,13 @@ def worker(rank, world, port, q):
     nl = shape[0] // world
     sim = SlabDiffusion(f0[rank * nl:(rank + 1) * nl].contiguous().cuda(), *args, transport="p2p")
     sim.step(steps)
+    sim.run(4)  # two steps per exchange: b2_diffusion3d_slab_halo2 push / ingest
     torch.cuda.synchronize()
     parts = [None] * world
     dist.all_gather_object(parts, sim.f.cpu().numpy())
     sim.close()
     if rank == 0:
-        ref = b2.Diffusion3D(f0.cuda(), *args).run(steps).cpu().numpy()
+        ref = b2.Diffusion3D(f0.cuda(), *args).run(steps + 4).cpu().numpy()
         q.put(bool(np.array_equal(np.concatenate(parts).view(np.uint32), ref.view(np.uint32))))
     dist.destroy_process_group()
 
