@@ -183,7 +183,10 @@ int b2_diffusion3d_slab_halo2(int nx_ext, int ny, int nz, int lo_h, int nx_local
  * exchanging faces through a library-owned mailbox); other L2-resident grids
  * in one cooperative launch; large grids two steps per HBM pass where the
  * planner finds a worthwhile tile (SOLOMON_DIFF_TEMPORAL=0: one step per
- * pass). All paths are bit-identical to nsteps single steps.
+ * pass). All paths are bit-identical to nsteps single steps. The first run of
+ * a large grid shape on a device times the planner's best few tile plans on
+ * f / fn (host-synchronising once; skipped while the stream is captured;
+ * SOLOMON_DIFF_AUTOTUNE=0 disables) and keeps the fastest.
  * *result_in_fn (if not NULL) is set to 1 when the final field is in fn, 0
  * when it is in f; the other buffer is scratch. */
 int b2_diffusion3d_run(int nx, int ny, int nz, float dx, float dy, float dz, float dt, float kappa,

@@ -418,7 +418,7 @@ int b2_diffusion3d_run(int nx, int ny, int nz, float dx, float dy, float dz, flo
   float* b = fn;
   int done = 0;
   TB2Plan tb;
-  if (use_tb && nsteps >= 2 && aligned && plan_tb2(nx, ny, nz, tb)) {
+  if (use_tb && nsteps >= 2 && aligned && plan_tb2_tuned(nx, ny, nz, c, f, fn, s, tb)) {
     for (; done + 2 <= nsteps; done += 2) {
       if (int rc = launch_tb2(tb, nx, ny, nz, c, a, b, s)) return rc;
       std::swap(a, b);

@@ -143,6 +143,8 @@ struct TB2Plan {
   size_t smem = 0;
 };
 bool plan_tb2(int nx, int ny, int nz, TB2Plan& best);
+bool plan_tb2_tuned(int nx, int ny, int nz, const Coefs& c, const float* f, float* fn, cudaStream_t s,
+                    TB2Plan& best);
 int launch_tb2(const TB2Plan& p, int nx, int ny, int nz, const Coefs& c, const float* f, float* fn, cudaStream_t s);
 
 // ---- shared-memory-resident time loop (diffusion_resident.cu) ----

@@ -8,7 +8,12 @@
 #include <cstddef>
 #include <cstdint>
 #include <cstdio>
+#include <map>
+#include <mutex>
+#include <tuple>
 #include <type_traits>
+#include <utility>
+#include <vector>
 
 #include "diffusion_common.cuh"
 
@@ -260,15 +265,16 @@ static bool tb2_instantiated(int S1, int S2) {
          (S1 == 6 && (S2 == 4 || S2 == 5 || S2 == 6));
 }
 
-bool plan_tb2(int nx, int ny, int nz, TB2Plan& best) {
-  if (nz % 4 != 0 || nx < 2) return false;
+// Every admissible (tile height, i-split) plan with its model score, best first.
+static std::vector<std::pair<double, TB2Plan>> tb2_candidates(int nx, int ny, int nz) {
+  std::vector<std::pair<double, TB2Plan>> out;
+  if (nz % 4 != 0 || nx < 2) return out;
   const int nz4 = nz / 4;
-  if ((32 * kTBWarps1) % nz4 != 0 || (32 * kTBWarps2) % nz4 != 0 || nz4 < 32) return false;  // row blocks, full warps
+  if ((32 * kTBWarps1) % nz4 != 0 || (32 * kTBWarps2) % nz4 != 0 || nz4 < 32) return out;  // row blocks, full warps
   const int blocks1 = 32 * kTBWarps1 / nz4, blocks2 = 32 * kTBWarps2 / nz4;
   const DeviceInfo& di = device_info();
   const size_t cap = static_cast<size_t>(di.smem_optin > 0 ? di.smem_optin : 227 * 1024);
   static const int force_tj = env_int("SOLOMON_DIFF_TB_TJ", 0);  // tuning knob (scripts/tb.sh sweeps)
-  double best_score = -1.0;
   for (int TJ = 1; TJ <= std::min(ny, 32); ++TJ) {
     if (force_tj && TJ != force_tj) continue;
     TB2Plan p;
@@ -295,17 +301,91 @@ bool plan_tb2(int nx, int ny, int nz, TB2Plan& best) {
       const double waves = std::ceil(static_cast<double>(q.grid) / di.sms);
       const double util = q.grid / (waves * di.sms);
       const double score = util * TJ / (TJ + 2.0) * static_cast<double>(q.IC) / (q.IC + 2.0);
-      if (score > best_score + 1e-9) {
-        best_score = score;
-        best = q;
-      }
+      out.emplace_back(score, q);
     }
   }
+  // best score first; ties keep the smaller tile / fewer splits (enumeration order)
+  std::stable_sort(out.begin(), out.end(),
+                   [](const std::pair<double, TB2Plan>& x, const std::pair<double, TB2Plan>& y) {
+                     return x.first > y.first + 1e-9;
+                   });
+  return out;
+}
+
+static void tb2_report(const char* what, int nx, int ny, int nz, const TB2Plan& p, double v) {
   static const bool verbose = env_int("SOLOMON_DIFF_TB_VERBOSE", 0) != 0;
-  if (verbose && best_score > 0)
-    std::fprintf(stderr, "tb2 plan %dx%dx%d: TJ=%d S=%d,%d IC=%d grid=%d smem=%zu score=%.4f\n", nx, ny, nz, best.TJ,
-                 best.S1, best.S2, best.IC, best.grid, best.smem, best_score);
-  return best_score > 0;
+  if (verbose)
+    std::fprintf(stderr, "tb2 plan %dx%dx%d: TJ=%d S=%d,%d IC=%d grid=%d smem=%zu %s=%.4f\n", nx, ny, nz, p.TJ, p.S1,
+                 p.S2, p.IC, p.grid, p.smem, what, v);
+}
+
+bool plan_tb2(int nx, int ny, int nz, TB2Plan& best) {
+  const auto c = tb2_candidates(nx, ny, nz);
+  if (c.empty()) return false;
+  best = c.front().second;
+  tb2_report("score", nx, ny, nz, best, c.front().first);
+  return true;
+}
+
+// On the first run of a grid shape, time the model's best few plans on the caller's own
+// buffers (f read, fn written: fn is scratch until the run writes it) and keep the
+// fastest for that shape and device. Every plan gives the same bits, so the choice only
+// moves time. Host-synchronising, hence skipped while the stream is being captured;
+// SOLOMON_DIFF_AUTOTUNE=0 keeps the model's pick.
+bool plan_tb2_tuned(int nx, int ny, int nz, const Coefs& c, const float* f, float* fn, cudaStream_t s,
+                    TB2Plan& best) {
+  static const int autotune = env_int("SOLOMON_DIFF_AUTOTUNE", 1);
+  static std::mutex mu;
+  static std::map<std::tuple<int, int, int, int>, TB2Plan> cache;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const auto key = std::make_tuple(nx, ny, nz, dev);
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = cache.find(key);
+    if (it != cache.end()) {
+      best = it->second;
+      return true;
+    }
+  }
+  const auto cand = tb2_candidates(nx, ny, nz);
+  if (cand.empty()) return false;
+  best = cand.front().second;
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  if (!autotune || cand.size() == 1 || cudaStreamIsCapturing(s, &cap) != cudaSuccess ||
+      cap != cudaStreamCaptureStatusNone) {
+    cudaGetLastError();
+    return true;  // model pick, not cached: a later uncaptured call may still tune
+  }
+  constexpr int kCandidates = 4;
+  cudaEvent_t ev[2];
+  if (cudaEventCreate(&ev[0]) != cudaSuccess || cudaEventCreate(&ev[1]) != cudaSuccess) {
+    cudaGetLastError();
+    return true;
+  }
+  float best_ms = 1e30f;
+  for (size_t i = 0; i < cand.size() && i < static_cast<size_t>(kCandidates); ++i) {
+    const TB2Plan& p = cand[i].second;
+    if (launch_tb2(p, nx, ny, nz, c, f, fn, s)) continue;  // warm-up (smem opt-in, caches)
+    cudaEventRecord(ev[0], s);
+    for (int r = 0; r < 2; ++r) launch_tb2(p, nx, ny, nz, c, f, fn, s);
+    cudaEventRecord(ev[1], s);
+    float ms = 0.f;
+    if (cudaEventSynchronize(ev[1]) != cudaSuccess || cudaEventElapsedTime(&ms, ev[0], ev[1]) != cudaSuccess) {
+      cudaGetLastError();
+      continue;
+    }
+    tb2_report("ms", nx, ny, nz, p, ms / 2);
+    if (ms < best_ms) {
+      best_ms = ms;
+      best = p;
+    }
+  }
+  cudaEventDestroy(ev[0]);
+  cudaEventDestroy(ev[1]);
+  std::lock_guard<std::mutex> lk(mu);
+  cache[key] = best;
+  return true;
 }
 
 template <int S1, int S2>
