@@ -52,10 +52,9 @@ struct TB2Args {
 
 constexpr int kTBWarps1 = 8, kTBWarps2 = 8;
 constexpr int kTBThreads = 32 * (1 + kTBWarps1 + kTBWarps2);
-// Every compute thread arrives on the ring mbarriers itself (release of its own
+// Every active compute thread arrives on the ring mbarriers itself (release of its own
 // shared-memory accesses): measured as fast as one elected lane per warp after
 // __syncwarp, and clean under compute-sanitizer racecheck.
-constexpr int kTBArrive = 32;
 
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
@@ -86,15 +85,17 @@ __global__ void __launch_bounds__(kTBThreads, 1) k_diffusion_tb2(const TB2Args a
   const int lo_in = max(qlo - 1, 0), hi_in = min(qhi + 1, nx - 1);    // input planes
   const int L = hi_in - lo_in + 1;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // active threads per compute role: whole row blocks of nz4 threads (nz4 % 32 == 0)
+  const int act1 = (32 * kTBWarps1 / nz4) * nz4, act2 = (32 * kTBWarps2 / nz4) * nz4;
 
   if (threadIdx.x == 0) {
     for (int k = 0; k < NST; ++k) {
       mbar_init(full_in + k, 1);
-      mbar_init(empty_in + k, kTBArrive * kTBWarps1);
+      mbar_init(empty_in + k, act1);
     }
     for (int k = 0; k < NS1; ++k) {
-      mbar_init(full_s1 + k, kTBArrive * kTBWarps1);
-      mbar_init(empty_s1 + k, kTBArrive * kTBWarps2);
+      mbar_init(full_s1 + k, act1);
+      mbar_init(empty_s1 + k, act2);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -130,6 +131,7 @@ __global__ void __launch_bounds__(kTBThreads, 1) k_diffusion_tb2(const TB2Args a
 
   if (warp <= kTBWarps1) {  // ---- step 1: s1 rows r = 0 .. <-> global j0-1+r (ring row r+1) ----
     const int tid = threadIdx.x - 32;
+    if (tid >= act1) return;  // whole idle warps when 256 is not a multiple of the row width
     auto in_slot = [&](int pl) { return in_ring + static_cast<size_t>((pl - lo_in) % NST) * in_floats; };
     auto wait_in = [&](int pl) { const int t = pl - lo_in; mbar_wait(full_in + t % NST, (t / NST) & 1); };
     const int c4 = tid % nz4, r0 = (tid / nz4) * S1;
@@ -203,6 +205,7 @@ __global__ void __launch_bounds__(kTBThreads, 1) k_diffusion_tb2(const TB2Args a
 
   // ---- step 2: output rows j0 + r2 (s1 row r2 + 1) ----
   const int tid = threadIdx.x - 32 * (1 + kTBWarps1);
+  if (tid >= act2) return;
   const int c4 = tid % nz4, r0 = (tid / nz4) * S2;
   const bool kfirst = c4 == 0, klast = c4 + 1 == nz4;
   unsigned int comp = 0;
@@ -270,7 +273,9 @@ static std::vector<std::pair<double, TB2Plan>> tb2_candidates(int nx, int ny, in
   std::vector<std::pair<double, TB2Plan>> out;
   if (nz % 4 != 0 || nx < 2) return out;
   const int nz4 = nz / 4;
-  if ((32 * kTBWarps1) % nz4 != 0 || (32 * kTBWarps2) % nz4 != 0 || nz4 < 32) return out;  // row blocks, full warps
+  // whole warps per row (a warp never spans two row blocks); rows wider than a role's threads
+  // do not fit, and threads past the last full row block idle
+  if (nz4 % 32 != 0 || nz4 > 32 * kTBWarps1 || nz4 > 32 * kTBWarps2) return out;
   const int blocks1 = 32 * kTBWarps1 / nz4, blocks2 = 32 * kTBWarps2 / nz4;
   const DeviceInfo& di = device_info();
   const size_t cap = static_cast<size_t>(di.smem_optin > 0 ? di.smem_optin : 227 * 1024);
@@ -281,9 +286,9 @@ static std::vector<std::pair<double, TB2Plan>> tb2_candidates(int nx, int ny, in
     p.TJ = TJ;
     p.S1 = (TJ + 2 + blocks1 - 1) / blocks1;
     p.S2 = (TJ + blocks2 - 1) / blocks2;
-    // TJ < 5 recomputes too many halo rows -- except on 1024-float rows, where one float4
-    // column per thread spans the row and TJ = 4 is the tallest tile that fits.
-    if (!tb2_instantiated(p.S1, p.S2) || TJ < (force_tj ? 1 : nz4 >= 256 ? 4 : 5)) continue;
+    // TJ < 5 recomputes too many halo rows -- except where one row block spans the row
+    // (rows of 768-1024 floats: 6 step-1 rows per thread) and TJ = 4 is the tallest tile.
+    if (!tb2_instantiated(p.S1, p.S2) || TJ < (force_tj ? 1 : blocks1 == 1 ? 4 : 5)) continue;
     p.R1 = std::max(blocks1 * p.S1, blocks2 * p.S2 + 2);  // step-1 rows written / read (one past the last)
     p.R = blocks1 * p.S1 + 2;                             // input rows read by step 1
     p.smem = 256 + (static_cast<size_t>(p.nst) * p.R + static_cast<size_t>(p.ns1) * p.R1) * nz * sizeof(float);

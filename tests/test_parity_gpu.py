@@ -316,7 +316,8 @@ def test_temporal_blocking_kernel_bit_identical(tmp_path):
         "args = (0.03, 0.02, 0.025, 2e-5, 1.0)\n"
         "for shape, steps in [((40, 37, 128), 4), ((13, 9, 512), 5), ((256, 64, 512), 6), ((66, 30, 1024), 2),\n"
         "                     ((300, 70, 256), 3), ((19, 131, 512), 4), ((9, 512, 128), 7), ((64, 5, 512), 2),\n"
-        "                     ((20, 37, 1024), 5), ((33, 4, 1024), 3)]:\n"
+        "                     ((20, 37, 1024), 5), ((33, 4, 1024), 3), ((17, 41, 384), 4), ((9, 23, 768), 3),\n"
+        "                     ((30, 50, 640), 2), ((12, 9, 896), 5)]:\n"
         "    f0 = np.random.default_rng(3).random(shape, dtype=np.float32)\n"
         "    want = oracle.Restatement().diffusion_run(f0, steps, *args)\n"
         "    got = b2.Diffusion3D(torch.from_numpy(f0).cuda(), *args).run(steps).cpu().numpy()\n"
