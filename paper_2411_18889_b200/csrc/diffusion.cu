@@ -26,6 +26,10 @@
 #include <cstddef>
 #include <cstdint>
 #include <cstdlib>
+#include <map>
+#include <mutex>
+#include <tuple>
+#include <vector>
 
 #include "diffusion_common.cuh"
 
@@ -312,6 +316,118 @@ static bool plan_march(int nx_out, int ny, int nz, MarchPlan& mp) {
   return true;
 }
 
+static int launch_march(const MarchPlan& mp, int nx, int ny, int nz, const Coefs& c, const float* f, const float* lo,
+                        const float* hi, float* fn, int i_begin, int i_end, cudaStream_t s) {
+  MarchArgs a{f, lo, hi, fn, nx, ny, nz, mp.TJ, mp.n_jtiles, i_begin, i_end, mp.IC, mp.nst, c};
+  switch (mp.S) {
+#define B2_MARCH_CASE(SV)                                                       \
+  case SV: {                                                                    \
+    allow_max_dynamic_smem(reinterpret_cast<const void*>(k_diffusion_march<SV>)); \
+    k_diffusion_march<SV><<<mp.grid, kMarchThreads, mp.smem, s>>>(a);           \
+    break;                                                                      \
+  }
+    B2_MARCH_CASE(1)
+    B2_MARCH_CASE(2)
+    B2_MARCH_CASE(4)
+    B2_MARCH_CASE(8)
+#undef B2_MARCH_CASE
+    default:
+      return B2_EINVAL;
+  }
+  return launch_status();
+}
+
+// A plan with S cells per thread, `occ` CTAs per SM of shared memory and `splits` i-splits
+// (0: fill one wave of occ x SMs).
+static bool plan_march_with(int nx_out, int ny, int nz, int S, int occ, int splits_req, MarchPlan& mp) {
+  if (nz % 4 != 0 || nz < 4) return false;
+  const int nz4 = nz / 4;
+  int TJ = std::min((kMarchThreads * S) / nz4, ny);
+  if (TJ < 1) return false;
+  static const int max_nst = std::max(2, env_int("SOLOMON_DIFF_NST", 3));
+  const size_t stage = static_cast<size_t>(TJ + 2) * nz * sizeof(float);
+  const int nst = static_cast<int>(std::min<size_t>(max_nst, ((228 * 1024) / occ - 1024 - 128) / stage));
+  if (nst < 2) return false;
+  mp = MarchPlan{};
+  mp.S = S, mp.TJ = TJ, mp.nst = nst, mp.smem = 128 + stage * nst;
+  mp.n_jtiles = (ny + TJ - 1) / TJ;
+  int splits = splits_req ? splits_req : std::max(1, occ * device_info().sms / mp.n_jtiles);
+  splits = std::min(splits, std::max(1, nx_out / 4));
+  mp.IC = (nx_out + splits - 1) / splits;
+  mp.grid = mp.n_jtiles * ((nx_out + mp.IC - 1) / mp.IC);
+  return true;
+}
+
+// On the first large step of a (planes, ny, nz) shape, time the default plan and a few
+// alternatives (2 or 4 cells per thread at the occupancy their launch bounds allow, a few
+// i-split counts) on the caller's buffers (f read, fn's planes [i_begin, i_end) written --
+// the step overwrites them) and keep the fastest: rows whose width leaves the default wave
+// under-filled (768 floats: 569 GLUPS) reach ~790. Same bits for every plan. Host-
+// synchronising once per shape and device; skipped under stream capture, for thin slabs,
+// when a SOLOMON_DIFF_{S,SPLITS,OCC} knob forces a plan, or with SOLOMON_DIFF_AUTOTUNE=0.
+static bool plan_march_tuned(int nx, int ny, int nz, const Coefs& c, const float* f, const float* lo,
+                             const float* hi, float* fn, int i_begin, int i_end, cudaStream_t s, MarchPlan& best) {
+  const int nx_out = i_end - i_begin;
+  if (!plan_march(nx_out, ny, nz, best)) return false;
+  static const bool tune = env_int("SOLOMON_DIFF_AUTOTUNE", 1) && !env_int("SOLOMON_DIFF_S", 0) &&
+                           !env_int("SOLOMON_DIFF_SPLITS", 0) && !std::getenv("SOLOMON_DIFF_OCC");
+  if (!tune || nx_out < 8) return true;
+  static std::mutex mu;
+  static std::map<std::tuple<int, int, int, int>, MarchPlan> cache;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const auto key = std::make_tuple(nx_out, ny, nz, dev);
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = cache.find(key);
+    if (it != cache.end()) {
+      best = it->second;
+      return true;
+    }
+  }
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(s, &cap) != cudaSuccess || cap != cudaStreamCaptureStatusNone) {
+    cudaGetLastError();
+    return true;
+  }
+  std::vector<MarchPlan> cand{best};
+  for (const int S : {2, 4}) {
+    for (const int splits : {0, 2, 3, 4}) {
+      MarchPlan q;
+      if (!plan_march_with(nx_out, ny, nz, S, S <= 2 ? 4 : 2, splits, q)) continue;
+      bool dup = false;
+      for (const MarchPlan& p : cand) dup |= p.S == q.S && p.TJ == q.TJ && p.IC == q.IC && p.nst == q.nst;
+      if (!dup) cand.push_back(q);
+    }
+  }
+  cudaEvent_t ev[2];
+  if (cudaEventCreate(&ev[0]) != cudaSuccess || cudaEventCreate(&ev[1]) != cudaSuccess) {
+    cudaGetLastError();
+    return true;
+  }
+  float best_ms = 1e30f;
+  for (const MarchPlan& p : cand) {
+    if (launch_march(p, nx, ny, nz, c, f, lo, hi, fn, i_begin, i_end, s)) continue;  // warm-up
+    cudaEventRecord(ev[0], s);
+    for (int r = 0; r < 2; ++r) launch_march(p, nx, ny, nz, c, f, lo, hi, fn, i_begin, i_end, s);
+    cudaEventRecord(ev[1], s);
+    float ms = 0.f;
+    if (cudaEventSynchronize(ev[1]) != cudaSuccess || cudaEventElapsedTime(&ms, ev[0], ev[1]) != cudaSuccess) {
+      cudaGetLastError();
+      continue;
+    }
+    if (ms < best_ms) {
+      best_ms = ms;
+      best = p;
+    }
+  }
+  cudaEventDestroy(ev[0]);
+  cudaEventDestroy(ev[1]);
+  std::lock_guard<std::mutex> lk(mu);
+  cache[key] = best;
+  return true;
+}
+
 static int launch_step(int nx, int ny, int nz, const Coefs& c, const float* f, const float* lo, const float* hi,
                        float* fn, int i_begin, int i_end, cudaStream_t s) {
   if (i_end <= i_begin) return B2_OK;
@@ -329,25 +445,8 @@ static int launch_step(int nx, int ny, int nz, const Coefs& c, const float* f, c
     k_diffusion_direct<<<grid, 256, 0, s>>>(f, lo, hi, fn, nx, ny, nz, i_begin, i_end, c);
     return launch_status();
   }
-  if (ok_align && plan_march(i_end - i_begin, ny, nz, mp)) {
-    MarchArgs a{f, lo, hi, fn, nx, ny, nz, mp.TJ, mp.n_jtiles, i_begin, i_end, mp.IC, mp.nst, c};
-    switch (mp.S) {
-#define B2_MARCH_CASE(SV)                                                       \
-  case SV: {                                                                    \
-    allow_max_dynamic_smem(reinterpret_cast<const void*>(k_diffusion_march<SV>)); \
-    k_diffusion_march<SV><<<mp.grid, kMarchThreads, mp.smem, s>>>(a);           \
-    break;                                                                      \
-  }
-      B2_MARCH_CASE(1)
-      B2_MARCH_CASE(2)
-      B2_MARCH_CASE(4)
-      B2_MARCH_CASE(8)
-#undef B2_MARCH_CASE
-      default:
-        return B2_EINVAL;
-    }
-    return launch_status();
-  }
+  if (ok_align && plan_march_tuned(nx, ny, nz, c, f, lo, hi, fn, i_begin, i_end, s, mp))
+    return launch_march(mp, nx, ny, nz, c, f, lo, hi, fn, i_begin, i_end, s);
   const size_t total = static_cast<size_t>(i_end - i_begin) * ny * nz;
   const int grid = static_cast<int>(std::min<size_t>((total + 255) / 256, 148 * 64));
   k_diffusion_generic<<<grid, 256, 0, s>>>(f, lo, hi, fn, nx, ny, nz, i_begin, i_end, c);
