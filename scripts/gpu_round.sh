@@ -8,7 +8,8 @@ python bench.py > gpurun_out/bench_$TAG.json 2> gpurun_out/bench_$TAG.err; tail 
 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/bench_ref_$TAG.json 2>&1
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_$TAG.csv python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-configs --dsteps 10 > /dev/null 2>&1
 ncu --set full --clock-control none --import-source on -k regex:k_force_fast -s 2 -c 1 -o gpurun_out/prof_force_$TAG python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-diffusion --no-configs > /dev/null 2>&1
-ncu --set full --clock-control none --import-source on -k regex:k_diffusion_march -s 40 -c 1 -o gpurun_out/prof_diff_$TAG python bench.py --steps 1 --warmup 0 --no-cpu-baseline --no-configs --dsteps 2 --particles 65536 > /dev/null 2>&1
+# k_diffusion_march at 512^3: the first launches time candidate plans (first step of the shape); launch 45 is a timed step
+ncu --set full --clock-control none --import-source on -k regex:k_diffusion_march -s 45 -c 1 -o gpurun_out/prof_diff_$TAG python scripts/time_diffusion.py 512 50 > /dev/null 2>&1
 # k_diffusion_tb2: launches 0-11 time the four candidate plans (first run of the shape), 12-13 are the chosen plan
 SOLOMON_DIFF_TEMPORAL=1 ncu --set full --clock-control none --import-source on -k regex:k_diffusion_tb2 -s 13 -c 1 -o gpurun_out/prof_tb2_$TAG python -c "
 import sys; sys.path.insert(0,'.')
