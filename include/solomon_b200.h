@@ -132,7 +132,11 @@ size_t b2_leapfrog_workspace_bytes(int n, int flags);
 
 /* --- 3D diffusion (listing_diffusion.c:1-25) --- */
 
-/* One explicit step fn = L(f) over the whole grid; f != fn. */
+/* One explicit step fn = L(f) over the whole grid; f != fn. The first large
+ * step of a shape on a device (here or through b2_diffusion3d_slab) times a
+ * few tile plans, writing fn, and keeps the fastest: one host
+ * synchronisation per shape, skipped under stream capture, identical bits
+ * for every plan (SOLOMON_DIFF_AUTOTUNE=0 disables). */
 int b2_diffusion3d(int nx, int ny, int nz, float dx, float dy, float dz, float dt, float kappa,
                    const float *f, float *fn, void *stream);
 
