@@ -175,6 +175,20 @@ def test_diffusion_vs_oracle_shapes(b2, restatement, shape):
     assert bits_equal(f.cpu().numpy(), want)
 
 
+@pytest.mark.parametrize("shape", [(40, 200, 768), (70, 100, 640), (24, 180, 1024), (20, 300, 701), (9, 513, 896)])
+def test_diffusion_march_single_steps_large(b2, restatement, shape):
+    """Grids past the direct kernel's L2 limit take the TMA plane march (nz % 4 == 0, with its
+    first-use plan timing) or the generic kernel; two single steps == the oracle, bit for bit."""
+    args = (0.01, 0.02, 0.015, 1e-5, 1.0)
+    f0 = np.random.default_rng(9).random(shape, dtype=np.float32)
+    want = restatement.diffusion_run(f0, 2, *args)
+    f = dev(f0)
+    fn = torch.empty_like(f)
+    b2.diffusion3d(*shape, *args, f, fn)
+    b2.diffusion3d(*shape, *args, fn, f)
+    assert bits_equal(f.cpu().numpy(), want)
+
+
 def test_diffusion_config1_128cube_100_steps(b2, restatement):
     """BASELINE config[1]: 128^3, 100 steps; bit-identical and mass-conserving."""
     n = 128
