@@ -173,7 +173,9 @@ def test_p2p_halo_random_slabs(tmp_path):
     assert np.load(out).all()
 
 
-def _p2p_run_worker(rank, world, port, counts, ny, nz, steps, out):
+def _p2p_run_worker(rank, world, port, counts, ny, nz, steps, out, lag=0.0):
+    import time
+
     import torch.distributed as dist
 
     import paper_2411_18889_b200 as b2
@@ -186,7 +188,14 @@ def _p2p_run_worker(rank, world, port, counts, ny, nz, steps, out):
     args = (0.03, 0.025, 0.02, 2e-5, 1.0)
     lo = sum(counts[:rank])
     sim = SlabDiffusion(torch.from_numpy(f0[lo:lo + counts[rank]]).cuda(), *args, transport="p2p")
-    sim.run(steps[0])
+    if lag:  # the last rank enqueues every exchange late: its neighbours' ingest waits in the GPU
+        for _ in range(steps[0] // 2):
+            if rank == world - 1:
+                time.sleep(lag)
+            sim.run(2)
+        steps = (steps[0] // 2 * 2, steps[1])
+    else:
+        sim.run(steps[0])
     sim.step(1)  # the per-step fused halo resumes from run()'s state
     sim.run(steps[1])
     torch.cuda.synchronize()
@@ -208,6 +217,17 @@ def test_p2p_run_two_steps_per_exchange(tmp_path, world, counts, ny, nz, steps):
 
     out = tmp_path / "run2.npz"
     mp.spawn(_p2p_run_worker, args=(world, _port(), counts, ny, nz, steps, str(out)), nprocs=world, join=True)
+    z = np.load(out)
+    assert np.array_equal(z["got"].view(np.uint32), z["want"].view(np.uint32))
+
+
+def test_p2p_run_waits_for_a_late_neighbour(tmp_path):
+    """run()'s two-plane exchange has no host barrier: a rank that enqueues each exchange 0.3 s
+    late makes its neighbour's ingest launch wait in the GPU; the result stays bit-identical."""
+    import torch.multiprocessing as mp
+
+    out = tmp_path / "runlag.npz"
+    mp.spawn(_p2p_run_worker, args=(2, _port(), (4, 5), 12, 64, (6, 2), str(out), 0.3), nprocs=2, join=True)
     z = np.load(out)
     assert np.array_equal(z["got"].view(np.uint32), z["want"].view(np.uint32))
 
