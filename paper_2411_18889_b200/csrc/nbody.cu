@@ -340,6 +340,11 @@ static const ForceVariant kVariants[] = {
 };
 #undef B2_FV
 
+static int env_int_nb(const char* name, int dflt) {
+  const char* e = std::getenv(name);
+  return e ? std::atoi(e) : dflt;
+}
+
 static int large_variant() {
   static int v = [] {
     const char* e = std::getenv("SOLOMON_NBODY_VARIANT");  // tuning knob (bench sweeps)
@@ -367,10 +372,13 @@ static int launch_partials(int Ni, const float4* ipos, int Nj, const float4* jpo
   // tuned large variant, else 64x8, else 64x2 (small N is latency-bound and
   // needs every warp it can get).
   const ForceVariant* v = &kVariants[large_variant()];
-  const long long want = 4LL * device_info().sms;
+  static const long long want_k = std::max(0, env_int_nb("SOLOMON_NBODY_WANT", 4));  // tuning knob: CTAs per SM
+  const long long want = want_k * device_info().sms;
   auto ctas = [&](const ForceVariant* c) { return (long long)((Ni + c->block * c->ipt - 1) / (c->block * c->ipt)) * nch; };
-  if (ctas(v) < want) v = &kVariants[1];
-  if (ctas(v) < want) v = &kVariants[10];
+  // below that, 64 x 8 only while it still gives >= 16 CTAs per SM; else 64 x 2 (N = 8192:
+  // 1598 vs 1455 Ginteractions/s, scripts/midn_sweep.py). Same per-lane arithmetic and j
+  // order in every variant, so the choice does not move a bit.
+  if (ctas(v) < want) v = ctas(&kVariants[1]) >= 4 * want ? &kVariants[1] : &kVariants[10];
   const int nit = (Ni + v->block * v->ipt - 1) / (v->block * v->ipt);
   v->fn[pot ? 1 : 0]<<<nit * nch, v->block, 0, s>>>(ipos, Ni, jpos, Nj, jchunk, nit, eps2, out);
   return launch_status();
