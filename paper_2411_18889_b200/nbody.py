@@ -96,7 +96,14 @@ class Leapfrog:
 
     One step: ``v += a h; x += v dt; a = calc_acc(x); v += a h`` with
     ``h = dt/2``. Steady state is two launches per step (force, fused update).
+    Up to 4736 particles the whole run is one persistent launch; between that and
+    ``GRAPH_MAX_N`` particles the per-step launches are the overhead, so ``step(k)``
+    (k >= 2) is captured once per k into a CUDA graph and replayed (``graphs=False``
+    turns that off; the same kernels run either way, so the results are identical).
     """
+
+    GRAPH_MIN_N = 4737
+    GRAPH_MAX_N = 1 << 15
 
     pos: torch.Tensor
     vel: torch.Tensor
@@ -104,6 +111,7 @@ class Leapfrog:
     dt: float
     potential: bool = False
     exact: bool = False
+    graphs: bool = True
 
     def __post_init__(self) -> None:
         n = self.pos.shape[0]
@@ -114,6 +122,7 @@ class Leapfrog:
         self._ws = torch.empty(max(int(load().b2_leapfrog_workspace_bytes(n, self._flags)), 16),
                                dtype=torch.uint8, device=self.pos.device)
         self.steps = 0
+        self._graphs: dict[int, torch.cuda.CUDAGraph] = {}
         self._run(0, init=True)
 
     def _run(self, nsteps: int, init: bool = False) -> None:
@@ -125,8 +134,33 @@ class Leapfrog:
                                      self._ws.numel(), stream_handle(self.pos.device)), "leapfrog")
 
     def step(self, nsteps: int = 1) -> None:
-        self._run(nsteps)
+        g = self._graph_for(nsteps)
+        if g is not None:
+            g.replay()
+        else:
+            self._run(nsteps)
         self.steps += nsteps
+
+    def _graph_for(self, nsteps: int):
+        """The captured ``b2_leapfrog(nsteps)`` for launch-bound sizes, else None."""
+        n = self.pos.shape[0]
+        if (not self.graphs or nsteps < 2 or not (self.GRAPH_MIN_N <= n <= self.GRAPH_MAX_N)
+                or torch.cuda.is_current_stream_capturing()):
+            return None
+        g = self._graphs.get(nsteps)
+        if g is None:
+            try:
+                g = torch.cuda.CUDAGraph()
+                side = torch.cuda.Stream(self.pos.device)
+                side.wait_stream(torch.cuda.current_stream(self.pos.device))
+                with torch.cuda.graph(g, stream=side):
+                    self._run(nsteps)  # recorded, not executed
+                torch.cuda.current_stream(self.pos.device).wait_stream(side)
+            except RuntimeError:  # capture refused: stay on direct launches
+                self.graphs = False
+                return None
+            self._graphs[nsteps] = g
+        return g
 
     def kernel_launches_per_step(self) -> int:
         return 2

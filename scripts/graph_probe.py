@@ -2,6 +2,13 @@
 import sys; sys.path.insert(0, '.')
 import torch, paper_2411_18889_b200 as b2
 for n in (8192, 16384, 32768):
+    for graphs in (False, True):
+        pos, vel = b2.plummer(n, 42)
+        lf = b2.Leapfrog(pos, vel, 2.0**-6, 2.0**-7, graphs=graphs)
+        lf.step(8); torch.cuda.synchronize()
+        e = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+        e[0].record(); lf.step(8); lf.step(8); lf.step(8); lf.step(8); e[1].record(); torch.cuda.synchronize()
+        print(f'n={n} Leapfrog(graphs={graphs}).step(8): {e[0].elapsed_time(e[1]) / 32 * 1e3:.1f} us/step')
     pos, vel = b2.plummer(n, 42)
     lf = b2.Leapfrog(pos, vel, 2.0**-6, 2.0**-7)
     lf.step(4); torch.cuda.synchronize()

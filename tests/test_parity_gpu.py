@@ -506,6 +506,22 @@ def test_leapfrog_persistent_small_n_bit_identical(tmp_path):
         assert bits_equal(res["1"][k], res["0"][k]), k
 
 
+def test_leapfrog_graph_replay_bit_identical(b2):
+    """Mid-N Leapfrog.step(k) replays a captured CUDA graph of b2_leapfrog(k); same kernels,
+    same bits as direct launches, across repeated and mixed step counts."""
+    pos, vel = b2.plummer(8192, 5)
+    a = b2.Leapfrog(pos.clone(), vel.clone(), 2.0 ** -6, 2.0 ** -7)
+    b = b2.Leapfrog(pos.clone(), vel.clone(), 2.0 ** -6, 2.0 ** -7, graphs=False)
+    for k in (4, 4, 3, 1, 4):
+        a.step(k)
+        b.step(k)
+    assert a._graphs and not b._graphs
+    torch.cuda.synchronize()
+    for x, y in ((a.pos, b.pos), (a.vel, b.vel), (a.acc, b.acc)):
+        assert bits_equal(x.cpu().numpy(), y.cpu().numpy())
+    assert a.steps == b.steps == 16
+
+
 def test_checkpoint_resume_single_device(b2, tmp_path):
     """Leapfrog (persistent small-N path) and Diffusion3D (resident path): N steps straight ==
     k steps + save + fresh driver from the checkpoint + N-k steps, bit for bit."""
