@@ -561,8 +561,8 @@ class SlabDiffusion:
     # ---- two steps per exchange ------------------------------------------------
     def run(self, nsteps: int) -> torch.Tensor:
         """Advance ``nsteps`` with TWO steps per halo exchange (collective, bit-identical to
-        ``step(nsteps)``). Each rank keeps a halo-extended copy of its slab with two neighbour
-        planes per side; a pass is one ``b2_diffusion3d_run(..., 2)`` over it (on large slabs
+        ``step(nsteps)``). ``f``/``fn`` are views of halo-extended slabs with two neighbour
+        planes per side; a pass is one ``b2_diffusion3d_run(..., 2)`` over a whole one (on large slabs
         the two-steps-per-HBM-pass kernel), the two planes next to the halo are exact after
         two steps and the two halo planes are refreshed between passes (NCCL send/recv, or
         over peer memory with ``b2_diffusion3d_slab_halo2`` for transport="p2p"). An odd
