@@ -6,7 +6,9 @@ reference counterpart; SURVEY.md §8f row 3 asks for energy / momentum diagnosti
 * energy: relative drift of E = K + W over S KDK steps (Plummer, standard units, E0 = -1/4);
 * momentum: |sum m v| stays at FP32 round-off of the initial (centre-of-mass frame) value;
 * reversibility: S/2 steps forward, velocities negated, S/2 steps back -> the initial
-  positions again up to FP32 round-off (leapfrog is time-symmetric).
+  positions again up to FP32 round-off (leapfrog is time-symmetric);
+* diffusion: a clamped-boundary eigenmode decays by the exact per-step factor, and the
+  zero-flux ends conserve the mean (256^3, 1000 steps through Diffusion3D.run).
 """
 import argparse
 import json
@@ -57,6 +59,25 @@ def main():
     back.step(half)
     err = float(((back.pos[:, :3] - pos[:, :3]).norm() / pos[:, :3].norm()).item())
     rows.append({"reversibility_relL2_pos": err, "steps_each_way": half})
+    print(json.dumps(rows[-1]), flush=True)
+    # diffusion: a clamped-boundary eigenmode decays by an exact factor per step
+    # (f = 1 + a cos(pi (i + 1/2) / nx) is an eigenvector of the listing's clamped stencil:
+    # lambda = 1 - 2 ce (1 - cos(pi / nx))), and the clamped (zero-flux) ends conserve the mean
+    g, dsteps = 256, 1000
+    dx = 1.0 / g
+    dargs = (dx, dx, dx, 0.1 * dx * dx, 1.0)
+    i = torch.arange(g, dtype=torch.float64, device="cuda")
+    mode = torch.cos(torch.pi * (i + 0.5) / g)
+    f0 = (1.0 + 0.5 * mode)[:, None, None].expand(g, g, g).contiguous()
+    sim = b2.Diffusion3D(f0.float(), *dargs)
+    sim.run(dsteps)
+    ce = 1.0 * dargs[3] / (dx * dx)
+    lam = 1.0 - 2.0 * ce * (1.0 - torch.cos(torch.tensor(torch.pi / g, dtype=torch.float64)))
+    want = 1.0 + 0.5 * lam ** dsteps * mode
+    got = sim.field.double().mean(dim=(1, 2))
+    rows.append({"diffusion_grid": g, "steps": dsteps, "decay_factor": float(lam ** dsteps),
+                 "mode_relL2": float(((got - want).norm() / (want - 1.0).norm()).item()),
+                 "mean_drift": float(abs(sim.field.double().mean().item() - 1.0))})
     print(json.dumps(rows[-1]), flush=True)
     if args.out:
         with open(args.out, "w") as fh:
