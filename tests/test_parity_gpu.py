@@ -189,6 +189,25 @@ def test_diffusion_march_single_steps_large(b2, restatement, shape):
     assert bits_equal(f.cpu().numpy(), want)
 
 
+def test_diffusion_eigenmode_decay(b2):
+    """Analytic check: f = 1 + cos(pi (i + 1/2) / nx) / 2 is an eigenvector of the listing's
+    clamped stencil, so each step scales the mode by 1 - 2 ce (1 - cos(pi / nx)); the
+    zero-flux ends keep the mean. 256 x 64 x 128 grid, 300 steps through Diffusion3D.run."""
+    nx, ny, nz, steps = 256, 64, 128, 300
+    dx = 1.0 / nx
+    args = (dx, dx, dx, 0.1 * dx * dx, 1.0)
+    i = torch.arange(nx, dtype=torch.float64, device="cuda")
+    mode = torch.cos(torch.pi * (i + 0.5) / nx)
+    f0 = (1.0 + 0.5 * mode)[:, None, None].expand(nx, ny, nz).contiguous().float()
+    got = b2.Diffusion3D(f0, *args).run(steps).double()
+    lam = 1.0 - 2.0 * 0.1 * (1.0 - np.cos(np.pi / nx))
+    want = 1.0 + 0.5 * lam ** steps * mode
+    prof = got.mean(dim=(1, 2))
+    assert float(((prof - want).norm() / (want - 1.0).norm()).item()) < 2e-5
+    assert abs(float(got.mean().item()) - 1.0) < 5e-6
+    assert float((got - prof[:, None, None]).abs().max().item()) == 0.0  # j, k stay uniform
+
+
 def test_diffusion_config1_128cube_100_steps(b2, restatement):
     """BASELINE config[1]: 128^3, 100 steps; bit-identical and mass-conserving."""
     n = 128
