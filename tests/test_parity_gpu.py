@@ -525,6 +525,21 @@ def test_leapfrog_persistent_small_n_bit_identical(tmp_path):
         assert bits_equal(res["1"][k], res["0"][k]), k
 
 
+@pytest.mark.parametrize("n", [4096, 8192])
+def test_leapfrog_time_reversible(b2, n):
+    """Leapfrog is time-symmetric: k steps forward, velocities negated, k steps back return
+    the initial positions to FP32 round-off (persistent one-launch path at 4096, graph-replayed
+    two-kernel path at 8192)."""
+    pos, vel = b2.plummer(n, 11)
+    fw = b2.Leapfrog(pos.clone(), vel.clone(), 2.0 ** -6, 2.0 ** -7)
+    fw.step(64)
+    fw.vel[:, :3].neg_()
+    back = b2.Leapfrog(fw.pos.clone(), fw.vel.clone(), 2.0 ** -6, 2.0 ** -7)
+    back.step(64)
+    err = float(((back.pos[:, :3] - pos[:, :3]).norm() / pos[:, :3].norm()).item())
+    assert err < 1e-5, err
+
+
 def test_leapfrog_graph_replay_bit_identical(b2):
     """Mid-N Leapfrog.step(k) replays a captured CUDA graph of b2_leapfrog(k); same kernels,
     same bits as direct launches, across repeated and mixed step counts."""
