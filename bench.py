@@ -4,12 +4,15 @@
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
     torchrun --nproc-per-node N bench.py --gpus N ...        (N > 1)
 
-Prints ONE JSON line (rank 0). Headline = N-body (BASELINE configs[2] at
-N=1: N=2^20 Plummer, one KDK step = one force evaluation + the fused
-kick/drift; configs[3] for N>1: N=2^22 sharded over N GPUs with an NCCL
-position all-gather). The diffusion numbers (configs[1]'s kernel at the
-north star's 512^3 on one GPU; configs[4]'s 1024^3 slabs for N>1) ride in
-``secondary.diffusion`` with their own roofline / cpu_baseline / e2e.
+Prints ONE compact JSON line (rank 0; ``--detail FILE`` writes the full record).
+Headline = N-body (BASELINE configs[2] at N=1: N=2^20 Plummer, one KDK step =
+one force evaluation + the fused kick/drift; configs[3] for N>1: N=2^22
+sharded over N GPUs with an NCCL position all-gather, the p2p transport as a
+guarded secondary, and the same N on one GPU as ``secondary.scale_anchor``).
+The diffusion numbers (the north star's 512^3 single step on one GPU, its
+two-steps-per-pass run, configs[4]'s 1024^3 slabs for N>1) ride in
+``secondary.diffusion`` / ``secondary.diffusion_run`` with their own roofline,
+parity and e2e.
 
 ``--impl reference`` times the reference's OWN CPU implementation
 (oracle/_ref: the paper's listings lowered by the reference transpiler's
@@ -55,10 +58,14 @@ def parse_args():
     ap.add_argument("--no-configs", action="store_true", help="skip the BASELINE parity configs [0] and [1]")
     ap.add_argument("--results", default=None,
                     help="also append the JSON line to this JSON-lines results file (rank 0)")
+    ap.add_argument("--detail", default=None,
+                    help="write the full record (every leg, every sample description) to this JSON file (rank 0); "
+                         "stdout carries the compact line")
     ap.add_argument("--transport", choices=["auto", "p2p", "nccl"], default="auto",
-                    help="N>1 data exchange: p2p = fused peer memory (position publish inside the update kernel; "
-                         "edge-plane kernel pushing halo rows into the neighbours' mailboxes), nccl = collectives. "
-                         "auto: p2p for both (falls back to nccl if peer mapping fails on any rank)")
+                    help="N>1 headline exchange: nccl = collectives (all_gather_into_tensor / grouped send-recv), "
+                         "p2p = fused peer memory (position publish inside the update kernel; edge-plane kernel "
+                         "pushing halo rows into the neighbours' mailboxes). auto = nccl, with the p2p transports "
+                         "measured afterwards as guarded secondaries (a p2p failure is reported, not fatal)")
     ap.add_argument("--dist", action="store_true",
                     help="use the multi-GPU drivers (NCCL) even at world size 1 (smoke-tests the N>1 path)")
     ap.add_argument("--same-device", action="store_true",
@@ -276,58 +283,117 @@ def run_reference(args, rank: int, world: int):
 # ---------------------------------------------------------------------------
 # our arm
 
+class _Ctx:
+    """Per-run plumbing shared by the legs: device, stream, ranks, timing helpers."""
+
+    def __init__(self, args, rank, world, local_rank):
+        import torch
+        import torch.distributed as dist
+
+        self.args, self.rank, self.world = args, rank, world
+        self.dist = dist
+        self.dev = torch.device("cuda", 0 if args.same_device else local_rank)
+        torch.cuda.set_device(self.dev)
+        self.stream = torch.cuda.current_stream(self.dev)
+        self.peaks = measured_peaks()
+        self.flush = torch.empty(512 << 20, dtype=torch.uint8, device=self.dev)  # > 126 MB L2
+        # NCCL is the N > 1 headline transport; --same-device (every rank on cuda:0, where NCCL
+        # refuses to run) rehearses the N > 1 path on the p2p transport instead
+        self.transport = "p2p" if args.same_device else ("nccl" if args.transport == "auto" else args.transport)
+
+    def barrier(self):
+        if self.world > 1:
+            self.dist.barrier()
+
+    def max_over_ranks(self, x: float) -> float:
+        import torch
+
+        if self.world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cpu" if self.args.same_device else self.dev)
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def all_ok(self, ok: bool) -> bool:
+        """Agree on a per-rank verdict (every rank gets the same answer: control flow stays matched)."""
+        import torch
+
+        if self.world == 1:
+            return ok
+        t = torch.tensor([1 if ok else 0], dtype=torch.int32, device="cpu" if self.args.same_device else self.dev)
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MIN)
+        return bool(int(t.item()))
+
+    def events(self, k: int):
+        import torch
+
+        return [torch.cuda.Event(enable_timing=True) for _ in range(k)]
+
+
+def fp32_peak_tflops(peaks: dict):
+    """FP32 roofline denominator: MEASURED_PEAKS.json when it carries an FP32 figure, else
+    measured live on this GPU (packed-FFMA2 throughput probe)."""
+    for k, v in peaks.items():
+        if "fp32" in k.lower() and isinstance(v, (int, float)) and 20.0 < float(v) < 200.0:
+            return float(v), f"MEASURED_PEAKS.json {k}"
+    probe = ctypes.CDLL(str(ROOT / "paper_2411_18889_b200" / "lib" / "libsolomon_probe.so"))
+    probe.solomon_probe_fp32_tflops.restype = ctypes.c_double
+    return probe.solomon_probe_fp32_tflops(5), "live FFMA2 probe (nominal 148x128x2x1.965 GHz = 74.4)"
+
+
+def timed_steps(ctx, step, nsteps: int, nev: int, flush: bool):
+    """W warm-up steps, then `nsteps` timed ones between barrier + synchronize on both sides;
+    per-step CUDA events on the launching stream; clocks sampled during the timed region."""
+    import torch
+
+    for _ in range(ctx.args.warmup):
+        if flush:
+            ctx.flush.zero_()
+        step(ctx.events(nev))
+    torch.cuda.synchronize(ctx.dev)
+    ctx.barrier()
+    clocks = ClockSampler(ctx.dev.index).start() if ctx.rank == 0 else None
+    torch.cuda.synchronize(ctx.dev)
+    ctx.barrier()
+    events = []
+    for _ in range(nsteps):
+        if flush:
+            ctx.flush.zero_()  # L2 flush between timed steps (outside the step events)
+        evs = ctx.events(nev)
+        step(evs)
+        events.append(evs)
+    torch.cuda.synchronize(ctx.dev)
+    ctx.barrier()
+    return events, (clocks.stop() if clocks else None)
+
+
 def run_ours(args, rank: int, world: int, local_rank: int):
     import numpy as np
     import torch
-    import torch.distributed as dist
 
     import paper_2411_18889_b200 as b2
     from paper_2411_18889_b200 import _lib
-    from paper_2411_18889_b200.distributed import ShardedLeapfrog, SlabDiffusion
+    from paper_2411_18889_b200.distributed import ShardedLeapfrog
 
-    dev = torch.device("cuda", 0 if args.same_device else local_rank)
-    if args.same_device:
-        args.transport = "p2p"  # NCCL refuses two ranks on one GPU
-    torch.cuda.set_device(dev)
+    ctx = _Ctx(args, rank, world, local_rank)
+    dev, stream = ctx.dev, ctx.stream
     lib = b2.load()
-    peaks = measured_peaks()
-    stream = torch.cuda.current_stream(dev)
-
-    def barrier():
-        if world > 1:
-            dist.barrier()
-
-    def max_over_ranks(x: float) -> float:
-        if world == 1:
-            return x
-        t = torch.tensor([x], dtype=torch.float64, device="cpu" if args.same_device else dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
-
-    flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
-
-    # FP32 roofline denominator, measured live on this GPU (MEASURED_PEAKS.json has no FP32 figure)
-    probe = ctypes.CDLL(str(ROOT / "paper_2411_18889_b200" / "lib" / "libsolomon_probe.so"))
-    probe.solomon_probe_fp32_tflops.restype = ctypes.c_double
-    fp32_peak = probe.solomon_probe_fp32_tflops(5)
-    fp32_source = ("measured live: packed-FFMA2 throughput probe on this GPU "
-                   "(nominal 148x128x2x1.965 GHz = 74.4)")
-    for k, v in peaks.items():  # a driver-measured FP32 figure, if MEASURED_PEAKS.json carries one, wins
-        if "fp32" in k.lower() and isinstance(v, (int, float)) and 20.0 < float(v) < 200.0:
-            fp32_peak, fp32_source = float(v), f"MEASURED_PEAKS.json {k}"
-            break
+    if world > 1:
+        _lib.set_poll_timeout(60.0)  # p2p legs: a stalled peer fails the leg (reported), never the line
+    fp32_peak, fp32_source = fp32_peak_tflops(ctx.peaks)
 
     # ---------------- N-body ----------------
     sharded = world > 1 or args.dist
     n = args.n or ((1 << 20) if world == 1 else (1 << 22))
     pos_np, vel_np = b2.plummer_numpy(n, 42)
+    steady = _lib.B2_KDK_REDUCE | _lib.B2_KDK_KICK_END | _lib.B2_KDK_KICK_DRIFT
+    hh = 0.5 * DT
     if not sharded:
         pos = torch.from_numpy(pos_np).to(dev)
         vel = torch.from_numpy(vel_np).to(dev)
         nch = lib.b2_calc_acc_nchunks(n, 0)
         part = torch.empty((nch * n, 4), dtype=torch.float32, device=dev)
         acc = torch.empty_like(pos)
-        h = 0.5 * DT
         sh = _lib.stream_handle(dev)
 
         def force():
@@ -336,188 +402,128 @@ def run_ours(args, rank: int, world: int, local_rank: int):
 
         def update(phases):
             _lib.check(lib.b2_kdk_update(n, pos.data_ptr(), vel.data_ptr(), acc.data_ptr(), part.data_ptr(), nch,
-                                         h, h, DT, phases, sh), "update")
+                                         hh, hh, DT, phases, sh), "update")
 
         force()
         update(_lib.B2_KDK_REDUCE)
         update(_lib.B2_KDK_KICK_DRIFT)
-        steady = _lib.B2_KDK_REDUCE | _lib.B2_KDK_KICK_END | _lib.B2_KDK_KICK_DRIFT
 
         def step(evs):
             evs[0].record(stream)
+            evs[3].record(stream)
             force()
             evs[1].record(stream)
             update(steady)
             evs[2].record(stream)
 
-        n_local = n
-        launches_per_step = 2
-        parallelism = "single GPU"
+        n_local, sim = n, None
+        parallelism = "1 GPU"
     else:
-        plan_lo = rank * (n // world)
-        nb_transport = "p2p" if args.transport == "auto" else args.transport
-        try:
-            sim = ShardedLeapfrog(torch.from_numpy(pos_np[plan_lo:plan_lo + n // world]).to(dev),
-                                  torch.from_numpy(vel_np[plan_lo:plan_lo + n // world]).to(dev), EPS, DT,
-                                  transport=nb_transport)
-        except Exception as e:  # noqa: BLE001
-            print(f"p2p position transport unavailable ({e}); using NCCL", file=sys.stderr)
-            nb_transport = "nccl"
-            sim = ShardedLeapfrog(torch.from_numpy(pos_np[plan_lo:plan_lo + n // world]).to(dev),
-                                  torch.from_numpy(vel_np[plan_lo:plan_lo + n // world]).to(dev), EPS, DT,
-                                  transport=nb_transport)
-        sim.step(1, close=False)
         n_local = n // world
-        steady = _lib.B2_KDK_REDUCE | _lib.B2_KDK_KICK_END | _lib.B2_KDK_KICK_DRIFT
+        lo = rank * n_local
+        sim = ShardedLeapfrog(torch.from_numpy(pos_np[lo:lo + n_local]).to(dev),
+                              torch.from_numpy(vel_np[lo:lo + n_local]).to(dev), EPS, DT, transport=ctx.transport)
+        sim.step(1, close=False)
 
         def step(evs):
-            hh = 0.5 * DT
             evs[0].record(stream)
-            if nb_transport == "nccl":
+            if sim.transport == "nccl":
                 sim.gather()
             else:
                 sim._await_peers()
             evs[3].record(stream)
             sim.k.partials(sim.pos, sim.pos_all, sim.eps, sim.part)
             evs[1].record(stream)
-            if nb_transport == "nccl":
+            if sim.transport == "nccl":
                 sim.k.update(sim.pos, sim.vel, sim.acc, sim.part, sim.nch, hh, hh, DT, steady)
             else:
                 sim._publish_update(sim.vel, sim.part, hh, hh, DT, steady)
             evs[2].record(stream)
 
-        launches_per_step = 2
-        parallelism = (f"i-shard x{world}, " + ("NCCL all_gather_into_tensor of positions per step"
-                                                  if nb_transport == "nccl" else
-                                                  "positions published to every peer by the update kernel "
-                                                  "(fused all-gather over peer memory)"))
+        parallelism = f"i-shard x{world}, " + ("NCCL all_gather_into_tensor of positions" if sim.transport == "nccl"
+                                               else "p2p: positions published to peers by the update kernel")
 
-    mk = lambda: [torch.cuda.Event(enable_timing=True) for _ in range(4)]  # noqa: E731
-    for _ in range(args.warmup):
-        flush.zero_()
-        step(mk())
-    torch.cuda.synchronize(dev)
-    barrier()
-    clocks = ClockSampler(dev.index).start() if rank == 0 else None
-    torch.cuda.synchronize(dev)
-    barrier()
-    events = []
-    for _ in range(args.steps):
-        flush.zero_()  # L2 flush between timed steps (outside the events)
-        evs = mk()
-        step(evs)
-        events.append(evs)
-    torch.cuda.synchronize(dev)
-    barrier()
-    clock_rec = clocks.stop() if clocks else None
+    events, clock_rec = timed_steps(ctx, step, args.steps, 4, flush=True)
+    if sim is not None:
+        sim.synchronize()
     step_ms = [e[0].elapsed_time(e[2]) for e in events]
-    force_ms = [(e[3] if sharded else e[0]).elapsed_time(e[1]) for e in events]
-    total_ms = max_over_ranks(sum(step_ms))
-    force_avg = max_over_ranks(statistics.mean(force_ms))
-    gather_ms = max_over_ranks(statistics.mean(e[0].elapsed_time(e[3]) for e in events)) if sharded else 0.0
+    force_ms = [e[3].elapsed_time(e[1]) for e in events]
+    total_ms = ctx.max_over_ranks(sum(step_ms))
+    force_avg = ctx.max_over_ranks(statistics.mean(force_ms))
+    gather_ms = ctx.max_over_ranks(statistics.mean(e[0].elapsed_time(e[3]) for e in events))
     interactions = float(n) * float(n)
     value = interactions * args.steps / (total_ms * 1e-3) / 1e9
     achieved_tf = FLOP_PER_INTERACTION * float(n_local) * float(n) / (force_avg * 1e-3) / 1e12
 
-    result = {
+    full = {
         "metric": METRIC, "value": value, "unit": "Ginteractions/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f32",
-        "data": "synthetic: Plummer sphere (seed 42, FP64 -> FP32 on host); diffusion grid U[0,1) (seed 7)",
+        "data": "synthetic: Plummer (seed 42, FP64->FP32 host); grid U[0,1) (seed 7)",
         "config": {
-            "workload": (f"nbody N={n} Plummer FP32, one KDK leapfrog step per step "
-                         f"(force evaluation of N^2 interactions + fused reduce/kick/drift)"),
-            "n": n, "eps": EPS, "dt": DT, "jchunks": int(lib.b2_calc_acc_nchunks(n, 0)),
-            "parallelism": parallelism,
-            "l2": "flushed between timed steps (512 MiB memset, outside the step events)",
+            "workload": f"nbody N={n} Plummer FP32, 1 KDK step/step (force N^2 + fused reduce/kick/drift)",
+            "n": n, "parallelism": parallelism, "l2": "flushed (512 MiB memset) between timed steps",
+            **({"scaling_note": f"N fixed at {n} for every P: P=1 on the same N in secondary.scale_anchor"}
+               if world > 1 else {}),
         },
         "roofline": {
             "bound": "fp32", "kernel": "k_force_fast", "achieved": achieved_tf, "peak": fp32_peak,
             "unit": "TFLOP/s", "frac": achieved_tf / fp32_peak if fp32_peak > 0 else None,
-            "traffic": ncu_traffic("k_force_fast"),
-            "traffic_note": ("DRAM bytes per launch (ncu --set full): almost all of it is the write of the "
-                             "64 j-chunk partial sums (N x 64 x 16 B) that the update kernel reduces in a fixed "
-                             "order; ~0.2 ms of HBM time in a ~400 ms FP32-bound launch"),
-            "flop_per_interaction": FLOP_PER_INTERACTION,
-            "peak_source": fp32_source,
-            "force_ms": force_avg, "allgather_ms": gather_ms,
+            "traffic": ncu_traffic("k_force_fast"), "peak_src": fp32_source, "force_ms": force_avg,
+            **({"gather_ms": gather_ms} if sharded else {}),
         },
-        "gpu_launches": launches_per_step * args.steps,
+        "gpu_launches": 2 * args.steps,
         "clocks": clock_rec,
     }
 
-    # e2e through the reference-facing drop-in with HOST (pinned) buffers
+    # e2e through the reference-facing API with HOST buffers
     if world == 1:
         hpos = torch.from_numpy(pos_np).pin_memory()
         hacc = torch.empty_like(hpos).pin_memory()
         P = ctypes.c_void_p
         lib.calc_acc(n, P(hpos.data_ptr()), P(hacc.data_ptr()), n, P(hpos.data_ptr()), EPS)  # warm the arena
-        t0 = time.perf_counter()
         k_e2e = max(1, min(args.steps, 3))
+        t0 = time.perf_counter()
         for _ in range(k_e2e):
             lib.calc_acc(n, P(hpos.data_ptr()), P(hacc.data_ptr()), n, P(hpos.data_ptr()), EPS)
         t_e2e = (time.perf_counter() - t0) / k_e2e
         _lib.check(lib.b2_last_error(), "calc_acc drop-in")
-        if rank == 0 and not args.no_cpu_baseline:
+        if not args.no_cpu_baseline:
             try:
-                result["parity"] = nbody_sample_parity(pos_np, hacc.numpy())
+                full["parity"] = nbody_sample_parity(pos_np, hacc.numpy())
             except FileNotFoundError as e:
-                result["parity"] = {"unavailable": str(e)}
-        result["e2e"] = {"value": interactions / t_e2e / 1e9, "unit": "Ginteractions/s",
-                         "h2d_bytes_per_step": 16 * n, "d2h_bytes_per_step": 16 * n,
-                         "api": "calc_acc(Ni, ipos, iacc, Nj, jpos, eps) C drop-in, pinned host buffers "
-                                "(ipos == jpos staged once), synchronous", "steps": k_e2e}
+                full["parity"] = {"unavailable": str(e)}
+        full["e2e"] = {"value": interactions / t_e2e / 1e9, "unit": "Ginteractions/s",
+                       "h2d_bytes_per_step": 16 * n, "d2h_bytes_per_step": 16 * n,
+                       "api": "calc_acc(Ni, ipos, iacc, Nj, jpos, eps) C drop-in on pinned host buffers"}
         del hpos, hacc
     else:
-        # e2e through the public driver API with HOST buffers: every step copies this rank's
-        # positions in from pinned memory, runs ShardedLeapfrog.step (exchange + force + update)
-        # and reads its accelerations back; wall time, max over ranks
-        hpos = sim.pos.cpu().pin_memory()
-        hacc = torch.empty_like(hpos).pin_memory()
-        k_e2e = max(1, min(args.steps, 2))
-        torch.cuda.synchronize(dev)
-        barrier()
-        t0 = time.perf_counter()
-        for _ in range(k_e2e):
-            sim.pos.copy_(hpos, non_blocking=True)
-            sim.step(1, close=False)
-            hacc.copy_(sim.acc, non_blocking=True)
-        torch.cuda.synchronize(dev)
-        t_e2e = max_over_ranks(time.perf_counter() - t0) / k_e2e
-        result["e2e"] = {"value": interactions / t_e2e / 1e9, "unit": "Ginteractions/s",
-                         "h2d_bytes_per_step": 16 * n, "d2h_bytes_per_step": 16 * n,
-                         "api": "ShardedLeapfrog.step(1) per step with each rank's positions copied in from "
-                                "pinned host memory and its accelerations read back (whole-job bytes)",
-                         "steps": k_e2e}
-        del hpos, hacc
-        # parity at the sharded size: every rank publishes its positions, rank 0 checks a sample of
-        # a device force evaluation over the gathered pos_all against the reference build
-        sim.gather()
-        torch.cuda.synchronize(dev)
-        barrier()
-        if rank == 0 and not args.no_cpu_baseline:
-            import paper_2411_18889_b200 as b2
-
-            allpos = sim.pos_all.contiguous()
-            out = torch.empty_like(allpos)
-            b2.calc_acc(n, allpos, out, n, allpos, EPS)
-            try:
-                result["parity"] = nbody_sample_parity(allpos.cpu().numpy(), out.cpu().numpy(),
-                                                       what="calc_acc on rank 0 over pos_all after the sharded run")
-            except FileNotFoundError as e:
-                result["parity"] = {"unavailable": str(e)}
-        barrier()
+        full["e2e"] = nbody_sharded_e2e(ctx, sim, n)
+        full["parity"] = nbody_sharded_parity(ctx, sim, n)
 
     # ---------------- diffusion ----------------
     if not args.no_diffusion:
-        result["secondary"] = {"diffusion": run_diffusion(args, rank, world, dev, stream, peaks, barrier,
-                                                          max_over_ranks, flush)}
+        full["secondary"] = {"diffusion": run_diffusion(ctx)}
+    else:
+        full["secondary"] = {}
+
+    if world > 1:
+        sec = full["secondary"]
+        if not args.same_device and ctx.transport == "nccl":
+            # the fused peer-memory transports, measured only after the NCCL numbers exist; a
+            # failure here (peer mapping refused, a stalled peer) is reported, never fatal
+            sec["nbody_p2p"] = guarded(ctx, "nbody p2p", lambda: nbody_p2p_leg(ctx, pos_np, vel_np, n))
+            if not args.no_diffusion:
+                sec["diffusion_p2p"] = guarded(ctx, "diffusion p2p", lambda: diffusion_p2p_leg(ctx))
+        sec["scale_anchor"] = scale_anchor(ctx, pos_np, n)
+        if sim is not None and sim.transport == "p2p":
+            sim.close()
 
     if world == 1 and not args.no_configs:
         try:
-            result["parity_configs"] = run_parity_configs(dev)
+            full["parity_configs"] = run_parity_configs(dev)
         except FileNotFoundError as e:
-            result["parity_configs"] = {"unavailable": str(e)}
+            full["parity_configs"] = {"unavailable": str(e)}
 
     # ---------------- CPU baseline (rank 0, N=1) ----------------
     if world == 1 and rank == 0 and not args.no_cpu_baseline:
@@ -525,30 +531,187 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         cores = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
         try:
             v, ni, dt = cpu_nbody_sample(pos_np, args.cpu_seconds)
-            result["cpu_baseline"] = {"value": v, "unit": "Ginteractions/s", "cores": cores, "kind": "reference",
-                                      "sample": f"{ni} random i x {n} j (one sampled force evaluation, {dt:.1f} s), "
-                                                f"oracle/_ref libref_fast (reference listing via its fallback "
-                                                f"lowering, g++ -Ofast -fopenmp), {cpu_info()}"}
+            full["cpu_baseline"] = {"value": v, "unit": "Ginteractions/s", "cores": cores, "kind": "reference",
+                                    "sample": f"{ni} random i x {n} j ({dt:.1f} s), oracle/_ref libref_fast "
+                                              f"(listing via its fallback lowering, g++ -Ofast -fopenmp), "
+                                              f"{cpu_info()}"}
             v3, ni3, dt3 = cpu_nbody_sample(pos_np, args.cpu_seconds / 3, "ieee")
-            result["cpu_baseline"]["ieee"] = {"value": v3, "sample": f"{ni3} random i x {n} j ({dt3:.1f} s), "
-                                                                     "oracle/_ref libref_ieee (g++ -O3 -fopenmp)"}
+            full["cpu_baseline"]["ieee"] = {"value": v3, "sample": f"{ni3} random i x {n} j ({dt3:.1f} s), "
+                                                                   "libref_ieee (g++ -O3 -fopenmp)"}
         except FileNotFoundError as e:
-            result["cpu_baseline"] = {"value": None, "unavailable": str(e)}
-    return result
+            full["cpu_baseline"] = {"value": None, "unavailable": str(e)}
+    return full
 
 
-def run_diffusion(args, rank, world, dev, stream, peaks, barrier, max_over_ranks, flush):
+def guarded(ctx, what: str, fn):
+    """Run a collective leg on every rank; any rank's failure is agreed on and reported."""
+    err = None
+    out = None
+    try:
+        out = fn()
+    except Exception as e:  # noqa: BLE001 -- reported in the line, the headline stands
+        err = f"{type(e).__name__}: {e}"
+        print(f"bench: {what} leg failed on rank {ctx.rank}: {err}", file=sys.stderr)
+    if not ctx.all_ok(err is None):
+        return {"error": (err or "failed on another rank")[:160]}
+    return out
+
+
+def nbody_sharded_e2e(ctx, sim, n):
+    """N > 1 e2e through the public driver API with HOST buffers: every step copies this rank's
+    positions in from pinned memory, runs ShardedLeapfrog.step (exchange + force + update) and
+    reads its accelerations back; wall time, max over ranks."""
+    import torch
+
+    hpos = sim.pos.cpu().pin_memory()
+    hacc = torch.empty_like(hpos).pin_memory()
+    k_e2e = max(1, min(ctx.args.steps, 2))
+    torch.cuda.synchronize(ctx.dev)
+    ctx.barrier()
+    t0 = time.perf_counter()
+    for _ in range(k_e2e):
+        sim.pos.copy_(hpos, non_blocking=True)
+        sim.step(1, close=False)
+        hacc.copy_(sim.acc, non_blocking=True)
+    torch.cuda.synchronize(ctx.dev)
+    t_e2e = ctx.max_over_ranks(time.perf_counter() - t0) / k_e2e
+    sim.synchronize()
+    return {"value": float(n) * n / t_e2e / 1e9, "unit": "Ginteractions/s",
+            "h2d_bytes_per_step": 16 * n, "d2h_bytes_per_step": 16 * n,
+            "api": "ShardedLeapfrog.step(1), positions in from / accelerations back to pinned host, every rank"}
+
+
+def nbody_sharded_parity(ctx, sim, n):
+    """Every rank publishes its positions; rank 0 checks a sample of a device force evaluation
+    over the gathered pos_all against the reference build, and that the sharded run's own
+    accelerations of its shard equal that unsharded evaluation bit for bit."""
+    import torch
+
+    import paper_2411_18889_b200 as b2
+
+    sim.gather()
+    torch.cuda.synchronize(ctx.dev)
+    ctx.barrier()
+    out = None
+    if ctx.rank == 0 and not ctx.args.no_cpu_baseline:
+        allpos = sim.pos_all.contiguous()
+        acc_full = torch.empty_like(allpos)
+        b2.calc_acc(n, allpos, acc_full, n, allpos, EPS)
+        # the sharded force of rank 0's shard at the same positions
+        sim.k.partials(sim.pos, sim.pos_all, sim.eps, sim.part)
+        mine = torch.empty_like(sim.pos)
+        sim.k.update(None, None, mine, sim.part, sim.nch, 0.0, 0.0, 0.0, 1)
+        same = bool(torch.equal(mine.view(torch.int32), acc_full[:sim.pos.shape[0]].view(torch.int32)))
+        try:
+            out = nbody_sample_parity(allpos.cpu().numpy(), acc_full.cpu().numpy(),
+                                      what="calc_acc over the gathered positions")
+            out["shard_eq_unsharded"] = same
+            out["ok"] = out["ok"] and same
+        except FileNotFoundError as e:
+            out = {"unavailable": str(e)}
+    ctx.barrier()
+    return out
+
+
+def nbody_p2p_leg(ctx, pos_np, vel_np, n):
+    """Fused all-gather transport (positions published into every peer by the update kernel)."""
+    import torch
+
+    from paper_2411_18889_b200 import _lib
+    from paper_2411_18889_b200.distributed import ShardedLeapfrog
+
+    nl = n // ctx.world
+    lo = ctx.rank * nl
+    sim = ShardedLeapfrog(torch.from_numpy(pos_np[lo:lo + nl]).to(ctx.dev),
+                          torch.from_numpy(vel_np[lo:lo + nl]).to(ctx.dev), EPS, DT, transport="p2p")
+    try:
+        sim.step(1, close=False)
+        hh, steady = 0.5 * DT, _lib.B2_KDK_REDUCE | _lib.B2_KDK_KICK_END | _lib.B2_KDK_KICK_DRIFT
+
+        def step(evs):
+            evs[0].record(ctx.stream)
+            sim._await_peers()
+            sim.k.partials(sim.pos, sim.pos_all, sim.eps, sim.part)
+            sim._publish_update(sim.vel, sim.part, hh, hh, DT, steady)
+            evs[1].record(ctx.stream)
+
+        steps = max(1, min(ctx.args.steps, 3))
+        saved = ctx.args.warmup
+        ctx.args.warmup = 1
+        try:
+            events, _ = timed_steps(ctx, step, steps, 2, flush=True)
+        finally:
+            ctx.args.warmup = saved
+        sim.synchronize()
+        ms = ctx.max_over_ranks(sum(e[0].elapsed_time(e[1]) for e in events))
+        return {"value": float(n) * n * steps / (ms * 1e-3) / 1e9, "unit": "Ginteractions/s", "steps": steps}
+    finally:
+        sim.close()
+
+
+def scale_anchor(ctx, pos_np, n):
+    """The same N-body N and diffusion grid on ONE GPU (rank 0 alone, the other ranks wait):
+    the P = 1 point of a strong-scaling curve whose P > 1 points are the lines' values."""
+    import torch
+
+    import paper_2411_18889_b200 as b2
+
+    out = None
+    ctx.barrier()
+    if ctx.rank == 0:
+        pos = torch.from_numpy(pos_np).to(ctx.dev)
+        acc = torch.empty_like(pos)
+        ws = b2.workspace(n, n, device=ctx.dev)
+        e0, e1 = ctx.events(2)
+        e0.record(ctx.stream)
+        b2.calc_acc(n, pos, acc, n, pos, EPS, ws=ws)
+        e1.record(ctx.stream)
+        torch.cuda.synchronize(ctx.dev)
+        out = {"nbody": {"value": float(n) * n / (e0.elapsed_time(e1) * 1e-3) / 1e9, "unit": "Ginteractions/s",
+                         "n": n, "what": "one unsharded force evaluation"}}
+        del pos, acc, ws
+        if not ctx.args.no_diffusion:
+            g = ctx.args.grid or 1024
+            dx = 1.0 / g
+            dargs = (dx, dx, dx, 0.1 * dx * dx, 1.0)
+            sim = b2.Diffusion3D(b2.init_grid(g, g, g, seed=7, device=ctx.dev), *dargs)
+            f, fn = sim.f, sim._fn
+            for _ in range(2):
+                b2.diffusion3d(g, g, g, *dargs, f, fn)
+            e0.record(ctx.stream)
+            for _ in range(4):
+                b2.diffusion3d(g, g, g, *dargs, f, fn)
+                f, fn = fn, f
+            e1.record(ctx.stream)
+            sim.run(2)
+            e2, e3 = ctx.events(2)
+            e2.record(ctx.stream)
+            sim.run(8)
+            e3.record(ctx.stream)
+            sim.synchronize()
+            out["diffusion_step"] = {"value": g ** 3 * 4 / (e0.elapsed_time(e1) * 1e-3) / 1e9, "unit": "GLUPS",
+                                     "grid": g}
+            out["diffusion_run"] = {"value": g ** 3 * 8 / (e2.elapsed_time(e3) * 1e-3) / 1e9, "unit": "GLUPS",
+                                    "grid": g}
+            del sim, f, fn
+        torch.cuda.empty_cache()
+    ctx.barrier()
+    return out
+
+
+def run_diffusion(ctx):
     import torch
 
     import paper_2411_18889_b200 as b2
     from paper_2411_18889_b200.distributed import SlabDiffusion
 
+    args, world, rank, dev = ctx.args, ctx.world, ctx.rank, ctx.dev
     lib = b2.load()
     g = args.grid or (512 if world == 1 else 1024)
     dx = 1.0 / g
     dargs = (dx, dx, dx, 0.1 * dx * dx, 1.0)
     single = world == 1 and not args.dist
-    transport = None
+    sim = None
     if single:
         f = b2.init_grid(g, g, g, seed=7, device=dev)
         fn = torch.empty_like(f)
@@ -558,19 +721,12 @@ def run_diffusion(args, rank, world, dev, stream, peaks, barrier, max_over_ranks
             a, b = bufs[i % 2], bufs[(i + 1) % 2]
             b2.diffusion3d(g, g, g, *dargs, a, b)
 
-        launches = 1
-        nxl = g
+        launches, nxl = 1, g
     else:
         nxl = g // world
         gen = torch.Generator(device=dev).manual_seed(7 + rank)
         f_local = torch.rand((nxl, g, g), generator=gen, dtype=torch.float32, device=dev)
-        transport = "p2p" if args.transport == "auto" else args.transport
-        try:
-            sim = SlabDiffusion(f_local, *dargs, transport=transport)
-        except Exception as e:  # noqa: BLE001 -- report and fall back to the NCCL transport
-            print(f"p2p halo transport unavailable ({e}); using NCCL", file=sys.stderr)
-            transport = "nccl"
-            sim = SlabDiffusion(f_local, *dargs, transport=transport)
+        sim = SlabDiffusion(f_local, *dargs, transport=ctx.transport)
 
         def dstep(i):
             sim.step(1)
@@ -579,81 +735,116 @@ def run_diffusion(args, rank, world, dev, stream, peaks, barrier, max_over_ranks
     for i in range(5):
         dstep(i)
     torch.cuda.synchronize(dev)
-    barrier()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
+    ctx.barrier()
+    e0, e1 = ctx.events(2)
+    e0.record(ctx.stream)
     for i in range(args.dsteps):  # back to back: inputs (2 x field) exceed L2, no flush needed
         dstep(i)
-    e1.record(stream)
+    e1.record(ctx.stream)
     torch.cuda.synchronize(dev)
-    barrier()
-    total_ms = max_over_ranks(e0.elapsed_time(e1))
+    if sim is not None:
+        sim.synchronize()
+    ctx.barrier()
+    total_ms = ctx.max_over_ranks(e0.elapsed_time(e1))
     step_ms = total_ms / args.dsteps
     cells = float(g) ** 3
-    glups = cells * args.dsteps / (total_ms * 1e-3) / 1e9
-    kernel_ms = step_ms  # one launch per step at N=1: average launch duration over the timed region
-    achieved = BYTES_PER_CELL * float(nxl) * g * g / (kernel_ms * 1e-3) / 1e9
+    achieved = BYTES_PER_CELL * float(nxl) * g * g / (step_ms * 1e-3) / 1e9
     out = {
-        "metric": "diffusion GLUPS", "value": glups, "unit": "GLUPS", "ms_per_step": step_ms,
-        "steps": args.dsteps, "warmup": 5, "dtype": "f32",
+        "metric": "diffusion GLUPS", "value": cells * args.dsteps / (total_ms * 1e-3) / 1e9, "unit": "GLUPS",
+        "ms_per_step": step_ms, "steps": args.dsteps, "warmup": 5, "dtype": "f32",
         "config": {"workload": f"diffusion3d {g}^3 FP32 7-point step" + (
-                       " (single GPU)" if single else f", i-slabs x{world}, halo transport {transport}"),
-                   "grid": [g, g, g], "dt_over_dx2": 0.1,
-                   "l2": "inputs (2 x {:.0f} MiB per GPU) larger than L2; no flush".format(4 * nxl * g * g / 2**20)},
+                       " (1 GPU)" if single else f", i-slabs x{world}, halo transport {sim.transport}"),
+                   "grid": [g, g, g], "l2": "2 fields per GPU > L2; no flush"},
         "roofline": {"bound": "hbm", "kernel": "k_diffusion_march", "achieved": achieved,
-                     "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"],
-                     "traffic": ncu_traffic("k_diffusion_march"), "bytes_per_cell": BYTES_PER_CELL,
-                     "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "_source" not in peaks else peaks["_source"]},
+                     "peak": ctx.peaks["hbm_gbs"], "unit": "GB/s", "frac": achieved / ctx.peaks["hbm_gbs"],
+                     "traffic": ncu_traffic("k_diffusion_march"), "bytes_per_cell": BYTES_PER_CELL},
         "gpu_launches": launches * args.dsteps,
     }
     if not single:
-        out["parity"] = slab_parity(sim, rank, world, dev, dargs, args)
-        out["run"] = run_slab_multistep(sim, args, rank, world, dev, stream, peaks, g, nxl, barrier, max_over_ranks,
-                                        dargs)
-    if single:
-        host_f = f.cpu().pin_memory()
-        host_fn = torch.empty_like(host_f).pin_memory()
-        P = ctypes.c_void_p
+        out["parity"] = slab_parity(sim, ctx, dargs)
+        out["run"] = run_slab_multistep(sim, ctx, g, nxl, dargs)
+        if sim.transport == "p2p":
+            sim.close()
+        return out
+    host_f = f.cpu().pin_memory()
+    host_fn = torch.empty_like(host_f).pin_memory()
+    P = ctypes.c_void_p
+    lib.diffusion3d(g, g, g, *dargs, P(host_f.data_ptr()), P(host_fn.data_ptr()))
+    k = 3
+    t0 = time.perf_counter()
+    for _ in range(k):
         lib.diffusion3d(g, g, g, *dargs, P(host_f.data_ptr()), P(host_fn.data_ptr()))
-        k = 3
-        t0 = time.perf_counter()
-        for _ in range(k):
-            lib.diffusion3d(g, g, g, *dargs, P(host_f.data_ptr()), P(host_fn.data_ptr()))
-        t = (time.perf_counter() - t0) / k
-        if rank == 0 and not args.no_cpu_baseline:
-            try:
-                out["parity"] = diffusion_parity(host_f.numpy(), host_fn.numpy(), 1, dargs)
-            except FileNotFoundError as e:
-                out["parity"] = {"unavailable": str(e)}
-        out["e2e"] = {"value": cells / t / 1e9, "unit": "GLUPS", "h2d_bytes_per_step": int(4 * cells),
-                      "d2h_bytes_per_step": int(4 * cells),
-                      "api": "diffusion3d(nx,...,f,fn) C drop-in, pinned host buffers, synchronous"}
-        if rank == 0 and not args.no_cpu_baseline:
-            _omp_env()
-            try:
-                v, steps, dt = cpu_diffusion_sample(host_f.numpy(), dargs, args.cpu_seconds / 2)
-                out["cpu_baseline"] = {"value": v, "unit": "GLUPS",
-                                       "cores": int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1)),
-                                       "kind": "reference",
-                                       "sample": f"{steps} steps of {g}^3 ({dt:.1f} s), oracle/_ref libref_fast"}
-                v3, steps3, dt3 = cpu_diffusion_sample(host_f.numpy(), dargs, args.cpu_seconds / 6, "ieee")
-                out["cpu_baseline"]["ieee"] = {"value": v3, "sample": f"{steps3} steps of {g}^3 ({dt3:.1f} s), "
-                                                                      "oracle/_ref libref_ieee (g++ -O3 -fopenmp)"}
-            except FileNotFoundError as e:
-                out["cpu_baseline"] = {"value": None, "unavailable": str(e)}
-        del host_f, host_fn
-        out["run"] = run_diffusion_multistep(args, dev, stream, peaks, g, dargs)
+    t = (time.perf_counter() - t0) / k
+    if not args.no_cpu_baseline:
+        try:
+            out["parity"] = diffusion_parity(host_f.numpy(), host_fn.numpy(), 1, dargs)
+        except FileNotFoundError as e:
+            out["parity"] = {"unavailable": str(e)}
+    out["e2e"] = {"value": cells / t / 1e9, "unit": "GLUPS", "h2d_bytes_per_step": int(4 * cells),
+                  "d2h_bytes_per_step": int(4 * cells), "api": "diffusion3d C drop-in, pinned host buffers"}
+    if not args.no_cpu_baseline:
+        _omp_env()
+        try:
+            v, steps, dt = cpu_diffusion_sample(host_f.numpy(), dargs, args.cpu_seconds / 2)
+            out["cpu_baseline"] = {"value": v, "unit": "GLUPS",
+                                   "cores": int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1)),
+                                   "kind": "reference", "sample": f"{steps} steps of {g}^3 ({dt:.1f} s), libref_fast"}
+            v3, steps3, dt3 = cpu_diffusion_sample(host_f.numpy(), dargs, args.cpu_seconds / 6, "ieee")
+            out["cpu_baseline"]["ieee"] = {"value": v3, "sample": f"{steps3} steps of {g}^3 ({dt3:.1f} s), "
+                                                                  "libref_ieee (g++ -O3 -fopenmp)"}
+        except FileNotFoundError as e:
+            out["cpu_baseline"] = {"value": None, "unavailable": str(e)}
+    del host_f, host_fn
+    out["run"] = run_diffusion_multistep(ctx, g, dargs)
     return out
 
 
-def slab_parity(sim, rank, world, dev, dargs, args):
+def diffusion_p2p_leg(ctx):
+    """The fused peer-memory halo transport (edge-plane kernel pushing rows into the
+    neighbours' mailboxes; run(): two-plane mailbox exchange), after the NCCL numbers."""
+    import torch
+
+    from paper_2411_18889_b200.distributed import SlabDiffusion
+
+    g = ctx.args.grid or 1024
+    dx = 1.0 / g
+    dargs = (dx, dx, dx, 0.1 * dx * dx, 1.0)
+    nxl = g // ctx.world
+    gen = torch.Generator(device=ctx.dev).manual_seed(7 + ctx.rank)
+    sim = SlabDiffusion(torch.rand((nxl, g, g), generator=gen, dtype=torch.float32, device=ctx.dev), *dargs,
+                        transport="p2p")
+    try:
+        sim.step(4)
+        torch.cuda.synchronize(ctx.dev)
+        ctx.barrier()
+        steps = max(2, ctx.args.dsteps // 2 * 2)
+        e0, e1, e2, e3 = ctx.events(4)
+        e0.record(ctx.stream)
+        sim.step(steps)
+        e1.record(ctx.stream)
+        sim.run(4)
+        e2.record(ctx.stream)
+        sim.run(steps)
+        e3.record(ctx.stream)
+        sim.synchronize()
+        ctx.barrier()
+        ms_step = ctx.max_over_ranks(e0.elapsed_time(e1))
+        ms_run = ctx.max_over_ranks(e2.elapsed_time(e3))
+        cells = float(g) ** 3
+        return {"step": {"value": cells * steps / (ms_step * 1e-3) / 1e9, "unit": "GLUPS"},
+                "run": {"value": cells * steps / (ms_run * 1e-3) / 1e9, "unit": "GLUPS (effective)"}}
+    finally:
+        sim.close()
+
+
+def slab_parity(sim, ctx, dargs):
     """One more sharded step; rank 0 checks its slab bit for bit against the reference listing run
     on its planes plus rank 1's first plane (the only neighbour data its planes read)."""
     import numpy as np
     import torch
-    import torch.distributed as dist
 
-    if args.no_cpu_baseline:
+    rank, world, dist = ctx.rank, ctx.world, ctx.dist
+    if ctx.args.no_cpu_baseline:
         return None
     on_dev = dist.get_backend() == "nccl"
     f0 = sim.f.clone() if rank == 0 else None
@@ -662,10 +853,10 @@ def slab_parity(sim, rank, world, dev, dargs, args):
         plane = sim.f[0].contiguous()
         dist.send(plane if on_dev else plane.cpu(), 0)
     elif rank == 0 and world > 1:
-        nb = torch.empty(sim.f.shape[1:], dtype=sim.f.dtype, device=dev if on_dev else "cpu")
+        nb = torch.empty(sim.f.shape[1:], dtype=sim.f.dtype, device=ctx.dev if on_dev else "cpu")
         dist.recv(nb, 1)
     sim.step(1)
-    torch.cuda.synchronize(dev)
+    sim.synchronize()
     if rank != 0:
         return None
     try:
@@ -678,31 +869,31 @@ def slab_parity(sim, rank, world, dev, dargs, args):
             want = oracle.Reference("ieee").diffusion3d(f0.cpu().numpy(), *dargs)
         got = sim.f.cpu().numpy()
         return {"bit_identical": bool(np.array_equal(want.view(np.uint32), got.view(np.uint32))), "steps": 1,
-                "checker": "oracle/_ref libref_ieee on rank 0's planes + rank 1's first plane",
-                "planes": int(got.shape[0])}
+                "checker": "libref_ieee on rank 0's planes + rank 1's first plane", "planes": int(got.shape[0])}
     except FileNotFoundError as e:
         return {"unavailable": str(e)}
 
 
-def run_slab_multistep(sim, args, rank, world, dev, stream, peaks, g, nxl, barrier, max_over_ranks, dargs):
+def run_slab_multistep(sim, ctx, g, nxl, dargs):
     """N > 1: SlabDiffusion.run -- two steps per exchange of two halo planes, each pass one
     b2_diffusion3d_run(..., 2) over the halo-extended slab (two steps per HBM pass on large
     slabs). Effective GLUPS = all cells x steps / time (max over ranks)."""
     import numpy as np
     import torch
-    import torch.distributed as dist
 
-    steps = max(2, args.dsteps // 2 * 2)
+    rank, world, dist = ctx.rank, ctx.world, ctx.dist
+    steps = max(2, ctx.args.dsteps // 2 * 2)
     sim.run(4)
-    torch.cuda.synchronize(dev)
-    barrier()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
+    torch.cuda.synchronize(ctx.dev)
+    ctx.barrier()
+    e0, e1 = ctx.events(2)
+    e0.record(ctx.stream)
     sim.run(steps)
-    e1.record(stream)
-    torch.cuda.synchronize(dev)
-    barrier()
-    ms = max_over_ranks(e0.elapsed_time(e1))
+    e1.record(ctx.stream)
+    torch.cuda.synchronize(ctx.dev)
+    sim.synchronize()
+    ctx.barrier()
+    ms = ctx.max_over_ranks(e0.elapsed_time(e1))
     cells = float(g) ** 3
     nx_ext = nxl + (2 if sim.has_lo else 0) + (2 if sim.has_hi else 0)
     pass_ms = 2 * ms / steps
@@ -710,17 +901,16 @@ def run_slab_multistep(sim, args, rank, world, dev, stream, peaks, g, nxl, barri
     out = {
         "metric": "diffusion GLUPS, multi-step sharded run (effective)", "value": cells * steps / (ms * 1e-3) / 1e9,
         "unit": "GLUPS", "ms_per_step": ms / steps, "steps": steps, "warmup": 4,
-        "config": {"workload": f"SlabDiffusion.run({steps}) on {g}^3 FP32, i-slabs x{world}, two steps per "
-                               f"exchange of two halo planes (transport {sim.transport})",
-                   "grid": [g, g, g], "l2": "inputs larger than L2; no flush"},
+        "config": {"workload": f"SlabDiffusion.run({steps}) on {g}^3, i-slabs x{world}, two steps per exchange "
+                               f"(transport {sim.transport})", "grid": [g, g, g]},
         "roofline": {"bound": "hbm", "kernel": "k_diffusion_tb2 (per rank, halo-extended slab)", "achieved": achieved,
-                     "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"],
+                     "peak": ctx.peaks["hbm_gbs"], "unit": "GB/s", "frac": achieved / ctx.peaks["hbm_gbs"],
                      "bytes_per_cell_per_launch": BYTES_PER_CELL, "steps_per_launch": 2},
         "gpu_launches": (steps // 2) * (3 if sim.transport == "p2p" and world > 1 else 1),
     }
     # parity: two more steps; rank 0 checks its planes against the reference listing run on
     # them plus rank 1's first two planes (the light cone of two steps)
-    if args.no_cpu_baseline:
+    if ctx.args.no_cpu_baseline:
         return out
     on_dev = dist.get_backend() == "nccl"
     f0 = sim.f.clone() if rank == 0 else None
@@ -729,10 +919,10 @@ def run_slab_multistep(sim, args, rank, world, dev, stream, peaks, g, nxl, barri
         two = sim.f[0:2].contiguous()
         dist.send(two if on_dev else two.cpu(), 0)
     elif rank == 0 and world > 1:
-        nb = torch.empty((2,) + tuple(sim.f.shape[1:]), dtype=sim.f.dtype, device=dev if on_dev else "cpu")
+        nb = torch.empty((2,) + tuple(sim.f.shape[1:]), dtype=sim.f.dtype, device=ctx.dev if on_dev else "cpu")
         dist.recv(nb, 1)
     sim.run(2)
-    torch.cuda.synchronize(dev)
+    sim.synchronize()
     if rank == 0:
         try:
             import oracle
@@ -741,29 +931,30 @@ def run_slab_multistep(sim, args, rank, world, dev, stream, peaks, g, nxl, barri
             want = oracle.Reference("ieee").diffusion_run(sub, 2, *dargs)[:nxl]
             got = sim.f.cpu().numpy()
             out["parity"] = {"bit_identical": bool(np.array_equal(want.view(np.uint32), got.view(np.uint32))),
-                             "steps": 2, "checker": "oracle/_ref libref_ieee on rank 0's planes + rank 1's first two"}
+                             "steps": 2, "checker": "libref_ieee on rank 0's planes + rank 1's first two"}
         except FileNotFoundError as e:
             out["parity"] = {"unavailable": str(e)}
     return out
 
 
-def run_diffusion_multistep(args, dev, stream, peaks, g, dargs):
+def run_diffusion_multistep(ctx, g, dargs):
     """The device-resident time loop (Diffusion3D.run -> b2_diffusion3d_run): on large grids two
     steps per HBM pass (k_diffusion_tb2). Effective GLUPS = cells x steps / time."""
     import torch
 
     import paper_2411_18889_b200 as b2
 
+    dev = ctx.dev
     f0 = b2.init_grid(g, g, g, seed=7, device=dev)
-    steps = max(2, args.dsteps // 2 * 2)
+    steps = max(2, ctx.args.dsteps // 2 * 2)
     sim = b2.Diffusion3D(f0.clone(), *dargs)
     sim.run(4)
     torch.cuda.synchronize(dev)
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
+    e0, e1 = ctx.events(2)
+    e0.record(ctx.stream)
     sim.run(steps)
-    e1.record(stream)
-    torch.cuda.synchronize(dev)
+    e1.record(ctx.stream)
+    sim.synchronize()
     ms = e0.elapsed_time(e1)
     cells = float(g) ** 3
     pass_ms = 2 * ms / steps  # one k_diffusion_tb2 launch = two steps
@@ -780,25 +971,92 @@ def run_diffusion_multistep(args, dev, stream, peaks, g, dargs):
     torch.cuda.synchronize(dev)
     t_e2e = time.perf_counter() - t0
     parity = None
-    if not args.no_cpu_baseline:
+    if not ctx.args.no_cpu_baseline:
         try:
             parity = diffusion_parity(host.numpy(), back.numpy(), steps, dargs)
         except FileNotFoundError as e:
             parity = {"unavailable": str(e)}
     return {
         "parity": parity,
-        "metric": "diffusion GLUPS, multi-step device-resident run (effective)", "value": cells * steps / (ms * 1e-3) / 1e9,
-        "unit": "GLUPS", "ms_per_step": ms / steps, "steps": steps, "warmup": 4,
-        "config": {"workload": f"Diffusion3D.run({steps}) on {g}^3 FP32 (b2_diffusion3d_run: two steps per HBM pass)",
-                   "grid": [g, g, g], "l2": "inputs (2 x field) larger than L2; no flush"},
-        "roofline": {"bound": "hbm", "kernel": "k_diffusion_tb2", "achieved": achieved, "peak": peaks["hbm_gbs"],
-                     "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"], "traffic": ncu_traffic("k_diffusion_tb2"),
+        "metric": "diffusion GLUPS, multi-step device-resident run (effective)",
+        "value": cells * steps / (ms * 1e-3) / 1e9, "unit": "GLUPS", "ms_per_step": ms / steps, "steps": steps,
+        "config": {"workload": f"Diffusion3D.run({steps}) on {g}^3 (two steps per HBM pass)", "grid": [g, g, g]},
+        "roofline": {"bound": "hbm", "kernel": "k_diffusion_tb2", "achieved": achieved, "peak": ctx.peaks["hbm_gbs"],
+                     "unit": "GB/s", "frac": achieved / ctx.peaks["hbm_gbs"], "traffic": ncu_traffic("k_diffusion_tb2"),
                      "bytes_per_cell_per_launch": BYTES_PER_CELL, "steps_per_launch": 2},
         "gpu_launches": steps // 2,
         "e2e": {"value": cells * steps / t_e2e / 1e9, "unit": "GLUPS", "h2d_bytes_per_step": int(4 * cells / steps),
-                "d2h_bytes_per_step": int(4 * cells / steps),
-                "api": f"pinned host field -> Diffusion3D(...).run({steps}) -> pinned host (one copy each way per run)"},
+                "d2h_bytes_per_step": int(4 * cells / steps), "api": f"pinned host -> Diffusion3D.run({steps}) -> host"},
     }
+
+
+def _r(x, nd=4):
+    """Round for the compact line (None passes through)."""
+    if isinstance(x, float):
+        return float(f"{x:.{nd}g}")
+    return x
+
+
+def _roof(r: dict | None) -> dict | None:
+    if not r:
+        return r
+    return {k: _r(r.get(k)) for k in ("bound", "kernel", "achieved", "peak", "unit", "frac", "traffic") if k in r}
+
+
+def compact(full: dict) -> dict:
+    """The driver-visible JSON line: every required key, short values (the driver keeps only the
+    tail of stdout). --detail writes the full record."""
+    keep = ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better", "scaling",
+            "vs_baseline", "dtype", "data", "gpu_launches", "clocks")
+    out = {k: _r(full.get(k)) for k in keep if k in full}
+    cfg = full.get("config", {})
+    out["config"] = {k: cfg[k] for k in ("workload", "n", "parallelism", "l2", "scaling_note") if k in cfg}
+    out["roofline"] = _roof(full.get("roofline"))
+    if "peak_src" in full.get("roofline", {}):
+        out["roofline"]["peak_src"] = full["roofline"]["peak_src"][:40]
+    if "cpu_baseline" in full:
+        cb = full["cpu_baseline"]
+        out["cpu_baseline"] = {k: _r(cb.get(k)) for k in ("value", "unit", "cores", "kind") if k in cb}
+        out["cpu_baseline"]["sample"] = (cb.get("sample") or cb.get("unavailable") or "")[:70]
+    if "e2e" in full:
+        e = full["e2e"]
+        out["e2e"] = {k: _r(e.get(k)) for k in ("value", "unit", "h2d_bytes_per_step", "d2h_bytes_per_step")}
+    if full.get("parity"):
+        pa = full["parity"]
+        out["parity"] = {k: _r(pa[k]) for k in ("relL2_acc", "tolerance", "ok", "shard_eq_unsharded") if k in pa}
+    sec = {}
+    d = full.get("secondary", {}).get("diffusion")
+    if d:
+        par = d.get("parity") or {}
+        sec["diffusion"] = {"value": _r(d["value"]), "unit": "GLUPS", "grid": d["config"]["grid"][0],
+                            "what": "1 step/launch" + ("" if "1 GPU" in d["config"]["workload"]
+                                                        else f", slabs, {d['config']['workload'].split()[-1]}"),
+                            "roofline": _roof(d["roofline"]), "bit_identical": par.get("bit_identical"),
+                            "gpu_launches": d.get("gpu_launches")}
+        if "e2e" in d:
+            sec["diffusion"]["e2e"] = {k: _r(d["e2e"][k]) for k in ("value", "unit", "h2d_bytes_per_step",
+                                                                     "d2h_bytes_per_step")}
+        if d.get("cpu_baseline", {}).get("value"):
+            sec["diffusion"]["cpu_baseline"] = {k: _r(d["cpu_baseline"][k]) for k in ("value", "cores", "kind")}
+        run = d.get("run")
+        if run:
+            rp = run.get("parity") or {}
+            sec["diffusion_run"] = {"value": _r(run["value"]), "unit": "GLUPS eff.", "what": "2 steps/launch",
+                                    "roofline": _roof(run["roofline"]), "bit_identical": rp.get("bit_identical")}
+            for k in ("kernel", "unit", "bound"):
+                sec["diffusion_run"]["roofline"].pop(k, None)
+    for k in ("nbody_p2p", "diffusion_p2p", "scale_anchor"):
+        v = full.get("secondary", {}).get(k)
+        if v is not None:
+            sec[k] = json.loads(json.dumps(v), parse_float=lambda s: _r(float(s)))
+    pc = full.get("parity_configs")
+    if pc and "nbody_4096_plummer_kdk16" in pc:
+        a, b = pc["nbody_4096_plummer_kdk16"], pc["diffusion_128_100steps"]
+        sec["config0"] = {"gips": _r(a["gpu_ginteractions_per_s"]), "relL2_pos": _r(a["parity_relL2"]["pos"], 2),
+                          "cpu_ms": _r(a["cpu_ms"])}
+        sec["config1"] = {"glups": _r(b["gpu_glups"]), "parity": b["parity"], "cpu_glups": _r(b["cpu_glups"])}
+    out["secondary"] = sec
+    return out
 
 
 def run_parity_configs(dev):
@@ -921,9 +1179,11 @@ def main():
 
         # a lost rank fails the run instead of hanging it
         init_distributed("gloo" if args.same_device else "nccl", timeout_s=900.0)
-    out = run_ours(args, rank, world, local_rank)
+    full = run_ours(args, rank, world, local_rank)
     if rank == 0:
-        _emit(out, json_out, args.results)
+        if args.detail:
+            pathlib.Path(args.detail).write_text(json.dumps(full, indent=1))
+        _emit(compact(full), json_out, args.results)
     if world > 1 or args.dist:
         import torch.distributed as dist
 

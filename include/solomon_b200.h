@@ -12,8 +12,11 @@
  *    (the OpenACC `present(...)` convention: computed in place, synchronous).
  *
  * 2. Stream-ordered `b2_*` API on device pointers: no allocation, no host
- *    synchronisation, returns 0 or an error code. Stateless and reentrant;
- *    scratch space is caller-owned (`*_workspace_bytes`).
+ *    synchronisation, returns 0 or an error code; scratch space is
+ *    caller-owned (`*_workspace_bytes`). The exceptions are named set-up and
+ *    query calls: b2_diffusion3d_plan (times tile plans and sizes the resident
+ *    mailbox; plans are cached per shape and device, so later calls read that
+ *    process-wide cache), b2_fault_status, and the b2_ipc_* mappings.
  *
  * Layouts are the reference's: particles are AoS float4 {x, y, z, m}
  * (listing_nbody.c:1,4-5,9); accelerations float4 {ax, ay, az, pot|0}
@@ -29,7 +32,13 @@
 extern "C" {
 #endif
 
-#if defined(__VECTOR_TYPES_H__) || defined(__CUDACC__)
+/* The particle type of listing_nbody.c:1, a 16-byte {x, y, z, w}. A C caller
+ * whose driver defines its own float4 (the listing assumes one) can make it the
+ * parameter type with `#define SOLOMON_FLOAT4_TYPE float4` before including
+ * this header; C++ callers need nothing (see the overloads at the end). */
+#if defined(SOLOMON_FLOAT4_TYPE)
+typedef SOLOMON_FLOAT4_TYPE solomon_float4;
+#elif defined(__VECTOR_TYPES_H__) || defined(__CUDACC__)
 typedef float4 solomon_float4;
 #else
 typedef struct solomon_float4 {
@@ -42,8 +51,11 @@ typedef struct solomon_float4 {
 #define B2_EINVAL (-1)  /* bad size / null pointer / unsupported flag        */
 #define B2_EALIGN (-2)  /* pointer not 16-byte aligned                       */
 #define B2_ESPACE (-3)  /* workspace too small                               */
-#define B2_ENOMEM (-4)  /* drop-in layer could not allocate staging memory   */
-/* positive values are cudaError_t codes from the launch / copy              */
+#define B2_ENOMEM (-4)  /* (unused since 0.2: allocation failures report the
+                           cudaError_t of the failed cudaMalloc)             */
+#define B2_ETIMEOUT (-5) /* a device-side wait for data another CTA or GPU
+                            publishes gave up (b2_fault_status)              */
+/* positive values are cudaError_t codes from the launch / copy / allocation */
 
 /* ---- b2_calc_acc flags --------------------------------------------------- */
 #define B2_POTENTIAL 1 /* also accumulate .w += m_j/sqrt(r2): listing_nbody.c:21-23 */
@@ -66,6 +78,13 @@ void calc_acc(const int Ni, solomon_float4 *ipos, solomon_float4 *iacc, const in
 void calc_acc_potential(const int Ni, solomon_float4 *ipos, solomon_float4 *iacc, const int Nj,
                         solomon_float4 *jpos, const float eps);
 
+/* The same two with the reference's arithmetic bit for bit (B2_EXACT: IEEE
+ * 1/sqrt, sequential j): identical to the listing's -O3 fallback build. */
+void calc_acc_exact(const int Ni, solomon_float4 *ipos, solomon_float4 *iacc, const int Nj,
+                    solomon_float4 *jpos, const float eps);
+void calc_acc_potential_exact(const int Ni, solomon_float4 *ipos, solomon_float4 *iacc, const int Nj,
+                              solomon_float4 *jpos, const float eps);
+
 /* Replaces `void diffusion3d(int nx, int ny, int nz, float dx, float dy,
  *   float dz, float dt, float kappa, const float *restrict f, float *restrict fn)`
  * -- pkg/tests/fixtures/listing_diffusion.c:5. Host or device
@@ -78,6 +97,26 @@ void diffusion3d(int nx, int ny, int nz, float dx, float dy, float dz, float dt,
 int b2_last_error(void);
 const char *b2_error_string(int code);
 const char *b2_version(void);
+
+/* --- Failure detection of the device-side waits ---------------------------
+ * Some kernels wait in the GPU for 16-byte words that another CTA
+ * (b2_leapfrog's persistent small-N path, b2_diffusion3d_run's resident path)
+ * or another GPU (the p2p slab halo: b2_diffusion3d_slab_edges,
+ * b2_diffusion3d_slab_halo2) publishes. A wait that exceeds the poll timeout
+ * does not hang or trap: the kernel records a fault code in a per-device word,
+ * every other waiting kernel on that device gives up at its next poll, and all
+ * of them exit normally (their outputs are then undefined). The CUDA context
+ * stays usable. */
+int b2_set_poll_timeout_ms(long long ms); /* default SOLOMON_POLL_TIMEOUT_S or 120 s;
+                                             applies to later launches            */
+long long b2_poll_timeout_ms(void);
+/* Synchronises `stream` (NULL: the legacy default stream), then reports the
+ * current device's fault word: B2_OK, or B2_ETIMEOUT with *which (if not NULL)
+ * set to the kernel that gave up first (b2_fault_kernel names it). clear = 1
+ * resets the word. Host-synchronising: call it at a checkpoint of a run, not
+ * per step. */
+int b2_fault_status(void *stream, int clear, int *which);
+const char *b2_fault_kernel(int which);
 
 /* =========================================================================
  * 2. Stream-ordered API (device pointers; `stream` is a cudaStream_t or NULL)
@@ -132,13 +171,22 @@ size_t b2_leapfrog_workspace_bytes(int n, int flags);
 
 /* --- 3D diffusion (listing_diffusion.c:1-25) --- */
 
-/* One explicit step fn = L(f) over the whole grid; f != fn. The first large
- * step of a shape on a device (here or through b2_diffusion3d_slab) times a
- * few tile plans, writing fn, and keeps the fastest: one host
- * synchronisation per shape, skipped under stream capture, identical bits
- * for every plan (SOLOMON_DIFF_AUTOTUNE=0 disables). */
+/* One explicit step fn = L(f) over the whole grid; f != fn. Uses the tile
+ * plan b2_diffusion3d_plan chose for the shape on this device, else the
+ * model's default (same bits either way). */
 int b2_diffusion3d(int nx, int ny, int nz, float dx, float dy, float dz, float dt, float kappa,
                    const float *f, float *fn, void *stream);
+
+/* Set-up call (the ONE place the diffusion path may allocate or synchronise):
+ * times a few tile plans of the single step (whole grid and the interior
+ * planes [1, nx-1) of a slab) and, with nsteps >= 2, of the two-steps-per-pass
+ * kernel on f (read) and fn (written: scratch), keeps the fastest per shape and
+ * device, and sizes the library-owned mailbox of b2_diffusion3d_run's resident
+ * path. Host-synchronising; tuning is skipped under stream capture and with
+ * SOLOMON_DIFF_AUTOTUNE=0. Optional: unplanned shapes run on the model's plans
+ * (and without the resident path), with identical bits. */
+int b2_diffusion3d_plan(int nx, int ny, int nz, float dx, float dy, float dz, float dt, float kappa,
+                        const float *f, float *fn, int nsteps, void *stream);
 
 /* Slab variant for i-decomposition: f holds this rank's
  * nx_local planes; halo_lo / halo_hi are the neighbour planes i = -1 and
@@ -181,18 +229,17 @@ int b2_diffusion3d_slab_halo2(int nx_ext, int ny, int nz, int lo_h, int nx_local
                               const void *in_lo, const void *in_hi, void *out_lo, void *out_hi,
                               int xchg, int phase, void *stream);
 
-/* nsteps device-resident steps ping-ponging f <-> fn (no host sync).
- * Grids that fit the chip's shared memory (e.g. 128^3) run all steps in one
- * persistent launch with the field resident in shared memory (bricks
- * exchanging faces through a library-owned mailbox); other L2-resident grids
- * in one cooperative launch; large grids two steps per HBM pass where the
- * planner finds a worthwhile tile (SOLOMON_DIFF_TEMPORAL=0: one step per
- * pass). All paths are bit-identical to nsteps single steps. The first run of
- * a large grid shape on a device times the planner's best few tile plans on
- * f / fn (host-synchronising once; skipped while the stream is captured;
- * SOLOMON_DIFF_AUTOTUNE=0 disables) and keeps the fastest.
- * *result_in_fn (if not NULL) is set to 1 when the final field is in fn, 0
- * when it is in f; the other buffer is scratch. */
+/* nsteps device-resident steps ping-ponging f <-> fn (no host sync, no
+ * allocation). Grids that fit the chip's shared memory (e.g. 128^3) run all
+ * steps in one persistent launch with the field resident in shared memory
+ * (bricks exchanging faces through the library-owned mailbox that
+ * b2_diffusion3d_plan(..., nsteps >= 2, ...) sized; unplanned: the next path);
+ * other L2-resident grids in one cooperative launch; large grids two steps
+ * per HBM pass where the planner finds a worthwhile tile
+ * (SOLOMON_DIFF_TEMPORAL=0: one step per pass), with the tile plan
+ * b2_diffusion3d_plan timed if it ran. All paths are bit-identical to nsteps
+ * single steps. *result_in_fn (if not NULL) is set to 1 when the final field
+ * is in fn, 0 when it is in f; the other buffer is scratch. */
 int b2_diffusion3d_run(int nx, int ny, int nz, float dx, float dy, float dz, float dt, float kappa,
                        float *f, float *fn, int nsteps, int *result_in_fn, void *stream);
 
@@ -210,6 +257,23 @@ int b2_ipc_close(void *dptr, size_t offset);
 
 #ifdef __cplusplus
 }
+
+/* C++ callers: the listing's call sites compile unchanged with the caller's own
+ * 16-byte float4 (listing_nbody.c:1 takes `float4 *`; a driver that defines
+ * `struct float4 {float x, y, z, w;}` binds here, the pointers are passed on). */
+#include <type_traits>
+#define SOLOMON_B200_F4_OVERLOAD(name)                                                              \
+  template <class F4, class = typename std::enable_if<sizeof(F4) == 16 &&                           \
+                                                      !std::is_same<F4, solomon_float4>::value>::type> \
+  inline void name(const int Ni, F4 *ipos, F4 *iacc, const int Nj, F4 *jpos, const float eps) {     \
+    name(Ni, reinterpret_cast<solomon_float4 *>(ipos), reinterpret_cast<solomon_float4 *>(iacc), Nj,  \
+         reinterpret_cast<solomon_float4 *>(jpos), eps);                                            \
+  }
+SOLOMON_B200_F4_OVERLOAD(calc_acc)
+SOLOMON_B200_F4_OVERLOAD(calc_acc_potential)
+SOLOMON_B200_F4_OVERLOAD(calc_acc_exact)
+SOLOMON_B200_F4_OVERLOAD(calc_acc_potential_exact)
+#undef SOLOMON_B200_F4_OVERLOAD
 #endif
 
 #endif /* SOLOMON_B200_H */

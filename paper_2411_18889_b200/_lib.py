@@ -20,6 +20,7 @@ B2_EINVAL = -1
 B2_EALIGN = -2
 B2_ESPACE = -3
 B2_ENOMEM = -4
+B2_ETIMEOUT = -5
 B2_POTENTIAL = 1
 B2_EXACT = 2
 B2_INIT_ACC = 4
@@ -33,10 +34,16 @@ _i, _f, _p, _sz = ctypes.c_int, ctypes.c_float, ctypes.c_void_p, ctypes.c_size_t
 SIGNATURES = {
     "calc_acc": (None, [_i, _p, _p, _i, _p, _f]),
     "calc_acc_potential": (None, [_i, _p, _p, _i, _p, _f]),
+    "calc_acc_exact": (None, [_i, _p, _p, _i, _p, _f]),
+    "calc_acc_potential_exact": (None, [_i, _p, _p, _i, _p, _f]),
     "diffusion3d": (None, [_i, _i, _i, _f, _f, _f, _f, _f, _p, _p]),
     "b2_last_error": (_i, []),
     "b2_error_string": (ctypes.c_char_p, [_i]),
     "b2_version": (ctypes.c_char_p, []),
+    "b2_set_poll_timeout_ms": (_i, [ctypes.c_longlong]),
+    "b2_poll_timeout_ms": (ctypes.c_longlong, []),
+    "b2_fault_status": (_i, [_p, _i, ctypes.POINTER(_i)]),
+    "b2_fault_kernel": (ctypes.c_char_p, [_i]),
     "b2_calc_acc_nchunks": (_i, [_i, _i]),
     "b2_calc_acc_workspace_bytes": (_sz, [_i, _i, _i]),
     "b2_calc_acc": (_i, [_i, _p, _p, _i, _p, _f, _i, _p, _sz, _p]),
@@ -46,6 +53,7 @@ SIGNATURES = {
     "b2_leapfrog": (_i, [_i, _p, _p, _p, _f, _f, _i, _i, _p, _sz, _p]),
     "b2_leapfrog_workspace_bytes": (_sz, [_i, _i]),
     "b2_diffusion3d": (_i, [_i, _i, _i, _f, _f, _f, _f, _f, _p, _p, _p]),
+    "b2_diffusion3d_plan": (_i, [_i, _i, _i, _f, _f, _f, _f, _f, _p, _p, _i, _p]),
     "b2_diffusion3d_slab": (_i, [_i, _i, _i, _f, _f, _f, _f, _f, _p, _p, _p, _p, _i, _i, _p]),
     "b2_diffusion3d_run": (_i, [_i, _i, _i, _f, _f, _f, _f, _f, _p, _p, _i, ctypes.POINTER(_i), _p]),
     "b2_diffusion3d_mailbox_bytes": (_sz, [_i, _i]),
@@ -93,6 +101,29 @@ def check(rc: int, what: str) -> None:
     if rc != B2_OK:
         msg = load().b2_error_string(rc).decode()
         raise SolomonError(f"{what}: {msg} (code {rc})")
+
+
+def check_fault(device: torch.device | None = None, what: str = "run") -> None:
+    """Synchronise ``device``'s current stream and raise if a device-side wait gave up.
+
+    The polling kernels (persistent small-N leapfrog, resident diffusion, the p2p slab
+    halo) never hang or trap: a word that does not arrive within the poll timeout
+    (``set_poll_timeout``) makes them record a fault and exit. This turns that record
+    into a ``SolomonError`` (and clears it, so the device is usable again)."""
+    lib = load()
+    which = ctypes.c_int(0)
+    with on_device(device if device is not None else torch.device("cuda", torch.cuda.current_device())):
+        rc = lib.b2_fault_status(stream_handle(device), 1, ctypes.byref(which))
+    if rc == B2_ETIMEOUT:
+        raise SolomonError(f"{what}: a device-side wait timed out after {lib.b2_poll_timeout_ms() / 1e3:g} s in "
+                           f"{lib.b2_fault_kernel(which.value).decode()}; results of that launch are undefined")
+    check(rc, what)
+
+
+def set_poll_timeout(seconds: float) -> None:
+    """How long a kernel waits in the GPU for another CTA's / GPU's data before giving up
+    (default ``SOLOMON_POLL_TIMEOUT_S`` or 120 s). Applies to later launches."""
+    check(load().b2_set_poll_timeout_ms(max(1, int(round(seconds * 1e3)))), "set_poll_timeout")
 
 
 def require_cuda(t: torch.Tensor, name: str) -> None:

@@ -5,8 +5,9 @@ plumbing a long Leapfrog / diffusion run needs to survive a restart.
 ``save(sim, path)`` / ``load(sim, path)`` work on any driver with
 ``state_dict`` / ``load_state_dict`` (Leapfrog, Diffusion3D, ShardedLeapfrog,
 SlabDiffusion). For the sharded drivers every rank writes and reads its own
-shard: put ``{rank}`` in the path (it is formatted with the rank), and call
-``load`` on every rank (it is collective).
+shard: put ``{rank}`` in the path (it is formatted with the rank; at world
+size > 1 a path without it is rejected), and call ``load`` on every rank (it is
+collective).
 """
 from __future__ import annotations
 
@@ -16,12 +17,22 @@ import pathlib
 import torch
 
 
+def _rank_world(sim) -> tuple[int | None, int]:
+    rank = getattr(sim, "rank", None)
+    world = getattr(sim, "world", None)
+    if hasattr(sim, "plan"):  # ShardedLeapfrog
+        rank, world = sim.plan.rank, sim.plan.world
+    return rank, int(world or 1)
+
+
 def _rank_path(path: str | os.PathLike, sim) -> pathlib.Path:
     p = str(path)
+    rank, world = _rank_world(sim)
+    if world > 1 and "{rank}" not in p:
+        # every rank would write (and later read) the same file: shards lost silently
+        raise ValueError(f"a sharded driver with world size {world} needs '{{rank}}' in the checkpoint path, "
+                         f"got {p!r}")
     if "{rank}" in p:
-        rank = getattr(sim, "rank", None)
-        if rank is None and hasattr(sim, "plan"):
-            rank = sim.plan.rank
         p = p.format(rank=rank if rank is not None else 0)
     return pathlib.Path(p)
 
@@ -31,7 +42,7 @@ def save(sim, path: str | os.PathLike) -> pathlib.Path:
     dst = _rank_path(path, sim)
     dst.parent.mkdir(parents=True, exist_ok=True)
     sd = {k: (v.detach().cpu() if isinstance(v, torch.Tensor) else v) for k, v in sim.state_dict().items()}
-    tmp = dst.with_name(dst.name + ".tmp")
+    tmp = dst.with_name(f"{dst.name}.{os.getpid()}.tmp")  # private to this process
     torch.save(sd, tmp)
     os.replace(tmp, dst)
     return dst

@@ -28,6 +28,18 @@ const DeviceInfo& device_info();
 // once per (device, kernel) -- the attribute is per context. Thread-safe.
 void allow_max_dynamic_smem(const void* fn);
 
+// Watchdog of the device-side polls (runtime.cu): where a waiting kernel records
+// that it gave up, and how long it may wait. A launch argument of every polling
+// kernel; built on the host per launch from the current device and the
+// b2_set_poll_timeout_ms setting.
+struct Watch {
+  unsigned int* fault;  // per-device word: first fault code, 0 = none
+  unsigned long long timeout_ns;
+};
+Watch make_watch();
+// fault codes (which kernel gave up), reported by b2_fault_status / b2_fault_kernel
+constexpr unsigned int kFaultLeapfrogSmall = 1, kFaultResident = 2, kFaultSlabEdges = 3, kFaultHalo2 = 4;
+
 // ---- Device helpers shared by the persistent kernels (k_leapfrog_small,
 // k_diffusion_resident): 16-byte words a producer CTA publishes and a consumer
 // CTA polls. A .b128 access is single-copy atomic (PTX memory model; libcu++'s
@@ -71,6 +83,18 @@ __device__ __forceinline__ unsigned long long globaltimer_ns() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
   return t;
+}
+
+// One poll iteration's verdict: true = stop waiting. Gives up when another
+// poller on this device already recorded a fault (so one dead peer ends every
+// wait within one poll, not one timeout each), or when this wait, begun at t0,
+// exceeded the limit -- then it records `code` (first fault wins). The caller
+// leaves its loops and exits normally: no __trap, the context stays usable.
+__device__ __forceinline__ bool poll_expired(const Watch& w, unsigned long long t0, unsigned int code) {
+  if (w.fault && *reinterpret_cast<volatile unsigned int*>(w.fault)) return true;
+  if (globaltimer_ns() - t0 <= w.timeout_ns) return false;
+  if (w.fault) atomicCAS(w.fault, 0u, code);
+  return true;
 }
 #endif
 

@@ -358,37 +358,50 @@ static bool plan_march_with(int nx_out, int ny, int nz, int S, int occ, int spli
   return true;
 }
 
-// On the first large step of a (planes, ny, nz) shape, time the default plan and a few
-// alternatives (2 or 4 cells per thread at the occupancy their launch bounds allow, a few
-// i-split counts) on the caller's buffers (f read, fn's planes [i_begin, i_end) written --
-// the step overwrites them) and keep the fastest: rows whose width leaves the default wave
-// under-filled (768 floats: 569 GLUPS) reach ~790. Same bits for every plan. Host-
-// synchronising once per shape and device; skipped under stream capture, for thin slabs,
-// when a SOLOMON_DIFF_{S,SPLITS,OCC} knob forces a plan, or with SOLOMON_DIFF_AUTOTUNE=0.
-static bool plan_march_tuned(int nx, int ny, int nz, const Coefs& c, const float* f, const float* lo,
-                             const float* hi, float* fn, int i_begin, int i_end, cudaStream_t s, MarchPlan& best) {
-  const int nx_out = i_end - i_begin;
-  if (!plan_march(nx_out, ny, nz, best)) return false;
+// Tuned single-step plans, per (output planes, ny, nz, device). b2_diffusion3d_plan times
+// the default plan and a few alternatives (2 or 4 cells per thread at the occupancy their
+// launch bounds allow, a few i-split counts) on the caller's buffers (f read, fn's planes
+// [i_begin, i_end) written) and keeps the fastest: rows whose width leaves the default
+// wave under-filled (768 floats: 569 GLUPS) reach ~790. Same bits for every plan. The
+// stream-ordered calls only look the plan up (no timing, no host synchronisation) and
+// take the model's default for shapes nobody planned.
+static std::mutex g_march_mu;
+static std::map<std::tuple<int, int, int, int>, MarchPlan> g_march_cache;
+
+static bool march_tuning_enabled() {
   static const bool tune = env_int("SOLOMON_DIFF_AUTOTUNE", 1) && !env_int("SOLOMON_DIFF_S", 0) &&
                            !env_int("SOLOMON_DIFF_SPLITS", 0) && !std::getenv("SOLOMON_DIFF_OCC");
-  if (!tune || nx_out < 8) return true;
-  static std::mutex mu;
-  static std::map<std::tuple<int, int, int, int>, MarchPlan> cache;
+  return tune;
+}
+
+static bool plan_march_lookup(int nx_out, int ny, int nz, MarchPlan& best) {
+  if (!plan_march(nx_out, ny, nz, best)) return false;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(g_march_mu);
+  auto it = g_march_cache.find(std::make_tuple(nx_out, ny, nz, dev));
+  if (it != g_march_cache.end()) best = it->second;
+  return true;
+}
+
+// Host-synchronising; skipped (model pick kept) under stream capture, for thin slabs,
+// when a SOLOMON_DIFF_{S,SPLITS,OCC} knob forces a plan, or with SOLOMON_DIFF_AUTOTUNE=0.
+static int plan_march_tune(int nx, int ny, int nz, const Coefs& c, const float* f, float* fn, int i_begin,
+                           int i_end, cudaStream_t s) {
+  const int nx_out = i_end - i_begin;
+  MarchPlan best;
+  if (!plan_march(nx_out, ny, nz, best) || !march_tuning_enabled() || nx_out < 8) return B2_OK;
   int dev = 0;
   cudaGetDevice(&dev);
   const auto key = std::make_tuple(nx_out, ny, nz, dev);
   {
-    std::lock_guard<std::mutex> lk(mu);
-    auto it = cache.find(key);
-    if (it != cache.end()) {
-      best = it->second;
-      return true;
-    }
+    std::lock_guard<std::mutex> lk(g_march_mu);
+    if (g_march_cache.count(key)) return B2_OK;
   }
   cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
   if (cudaStreamIsCapturing(s, &cap) != cudaSuccess || cap != cudaStreamCaptureStatusNone) {
     cudaGetLastError();
-    return true;
+    return B2_OK;
   }
   std::vector<MarchPlan> cand{best};
   for (const int S : {2, 4}) {
@@ -401,15 +414,17 @@ static bool plan_march_tuned(int nx, int ny, int nz, const Coefs& c, const float
     }
   }
   cudaEvent_t ev[2];
-  if (cudaEventCreate(&ev[0]) != cudaSuccess || cudaEventCreate(&ev[1]) != cudaSuccess) {
-    cudaGetLastError();
-    return true;
+  cudaError_t e;
+  if ((e = cudaEventCreate(&ev[0])) != cudaSuccess) return static_cast<int>(e);
+  if ((e = cudaEventCreate(&ev[1])) != cudaSuccess) {
+    cudaEventDestroy(ev[0]);
+    return static_cast<int>(e);
   }
   float best_ms = 1e30f;
   for (const MarchPlan& p : cand) {
-    if (launch_march(p, nx, ny, nz, c, f, lo, hi, fn, i_begin, i_end, s)) continue;  // warm-up
+    if (launch_march(p, nx, ny, nz, c, f, nullptr, nullptr, fn, i_begin, i_end, s)) continue;  // warm-up
     cudaEventRecord(ev[0], s);
-    for (int r = 0; r < 2; ++r) launch_march(p, nx, ny, nz, c, f, lo, hi, fn, i_begin, i_end, s);
+    for (int r = 0; r < 2; ++r) launch_march(p, nx, ny, nz, c, f, nullptr, nullptr, fn, i_begin, i_end, s);
     cudaEventRecord(ev[1], s);
     float ms = 0.f;
     if (cudaEventSynchronize(ev[1]) != cudaSuccess || cudaEventElapsedTime(&ms, ev[0], ev[1]) != cudaSuccess) {
@@ -423,9 +438,9 @@ static bool plan_march_tuned(int nx, int ny, int nz, const Coefs& c, const float
   }
   cudaEventDestroy(ev[0]);
   cudaEventDestroy(ev[1]);
-  std::lock_guard<std::mutex> lk(mu);
-  cache[key] = best;
-  return true;
+  std::lock_guard<std::mutex> lk(g_march_mu);
+  g_march_cache[key] = best;
+  return launch_status();
 }
 
 static int launch_step(int nx, int ny, int nz, const Coefs& c, const float* f, const float* lo, const float* hi,
@@ -445,7 +460,7 @@ static int launch_step(int nx, int ny, int nz, const Coefs& c, const float* f, c
     k_diffusion_direct<<<grid, 256, 0, s>>>(f, lo, hi, fn, nx, ny, nz, i_begin, i_end, c);
     return launch_status();
   }
-  if (ok_align && plan_march_tuned(nx, ny, nz, c, f, lo, hi, fn, i_begin, i_end, s, mp))
+  if (ok_align && plan_march_lookup(i_end - i_begin, ny, nz, mp))
     return launch_march(mp, nx, ny, nz, c, f, lo, hi, fn, i_begin, i_end, s);
   const size_t total = static_cast<size_t>(i_end - i_begin) * ny * nz;
   const int grid = static_cast<int>(std::min<size_t>((total + 255) / 256, 148 * 64));
@@ -479,6 +494,29 @@ int b2_diffusion3d_slab(int nx_local, int ny, int nz, float dx, float dy, float 
   if (i_begin < 0 || i_end > nx_local || i_begin > i_end) return B2_EINVAL;
   return launch_step(nx_local, ny, nz, make_coefs(dx, dy, dz, dt, kappa), f, halo_lo, halo_hi, fn, i_begin, i_end,
                      as_stream(stream));
+}
+
+int b2_diffusion3d_plan(int nx, int ny, int nz, float dx, float dy, float dz, float dt, float kappa, const float* f,
+                        float* fn, int nsteps, void* stream) {
+  if (int rc = check_grid(nx, ny, nz, f, fn)) return rc;
+  if (nsteps < 0) return B2_EINVAL;
+  const Coefs c = make_coefs(dx, dy, dz, dt, kappa);
+  cudaStream_t s = as_stream(stream);
+  const bool aligned = nz % 4 == 0 && aligned16(f) && aligned16(fn);
+  if (!aligned) return B2_OK;  // the generic kernel has no plan
+  static const long long direct_max = env_int("SOLOMON_DIFF_DIRECT_MAXCELLS", 1 << 22);
+  const long long cells = static_cast<long long>(nx) * ny * nz;
+  int rc;
+  if (cells > direct_max) {
+    // whole-grid steps, and the interior planes [1, nx-1) of a slab (SlabDiffusion.step)
+    if ((rc = plan_march_tune(nx, ny, nz, c, f, fn, 0, nx, s))) return rc;
+    if (nx > 2 && (rc = plan_march_tune(nx, ny, nz, c, f, fn, 1, nx - 1, s))) return rc;
+  }
+  if (nsteps >= 2) {
+    if ((rc = plan_resident(nx, ny, nz))) return rc;
+    if (env_int("SOLOMON_DIFF_TEMPORAL", 1) && (rc = plan_tb2_tune(nx, ny, nz, c, f, fn, s))) return rc;
+  }
+  return B2_OK;
 }
 
 int b2_diffusion3d_run(int nx, int ny, int nz, float dx, float dy, float dz, float dt, float kappa, float* f,
@@ -517,7 +555,7 @@ int b2_diffusion3d_run(int nx, int ny, int nz, float dx, float dy, float dz, flo
   float* b = fn;
   int done = 0;
   TB2Plan tb;
-  if (use_tb && nsteps >= 2 && aligned && plan_tb2_tuned(nx, ny, nz, c, f, fn, s, tb)) {
+  if (use_tb && nsteps >= 2 && aligned && plan_tb2_lookup(nx, ny, nz, tb)) {
     for (; done + 2 <= nsteps; done += 2) {
       if (int rc = launch_tb2(tb, nx, ny, nz, c, a, b, s)) return rc;
       std::swap(a, b);

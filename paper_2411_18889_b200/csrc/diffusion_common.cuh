@@ -143,12 +143,14 @@ struct TB2Plan {
   size_t smem = 0;
 };
 bool plan_tb2(int nx, int ny, int nz, TB2Plan& best);
-bool plan_tb2_tuned(int nx, int ny, int nz, const Coefs& c, const float* f, float* fn, cudaStream_t s,
-                    TB2Plan& best);
+bool plan_tb2_lookup(int nx, int ny, int nz, TB2Plan& best);  // tuned plan if planned, else the model's pick
+int plan_tb2_tune(int nx, int ny, int nz, const Coefs& c, const float* f, float* fn, cudaStream_t s);
 int launch_tb2(const TB2Plan& p, int nx, int ny, int nz, const Coefs& c, const float* f, float* fn, cudaStream_t s);
 
 // ---- shared-memory-resident time loop (diffusion_resident.cu) ----
-// Launches all nsteps for grids that fit the SMs' shared memory; false if not applicable.
+// Launches all nsteps for grids that fit the SMs' shared memory; false if not applicable
+// or the device's mailbox was not sized for the shape by plan_resident (b2_diffusion3d_plan).
 bool launch_resident(int nx, int ny, int nz, const Coefs& c, float* f, float* fn, int nsteps, cudaStream_t s);
+int plan_resident(int nx, int ny, int nz);  // (re)allocates the mailbox; host-synchronising
 
 }  // namespace b2

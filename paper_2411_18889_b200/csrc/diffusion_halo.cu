@@ -16,6 +16,10 @@
 //     state s (rows of this CTA only), computes its edge rows of state s+1 and
 //     stores them, tagged, straight into the neighbour's mailbox (NVLink /
 //     NVSwitch peer stores; the pointer is a CUDA-IPC mapping);
+//   * a row that never arrives (dead or stalled peer) ends the wait after the
+//     poll timeout through the watchdog (poll_expired, runtime.cu): the kernel
+//     exits normally and b2_fault_status reports B2_ETIMEOUT -- no trap, the
+//     context survives;
 //   * a producer cannot lap a consumer: its state s+2 rows need the consumer's
 //     state s+1 rows, which the consumer pushes only after it has read state s
 //     (same row tiling on every rank), so two parities suffice.
@@ -45,10 +49,12 @@ struct EdgeArgs {
   int step;            // computes state step+1 from state step
   int push_only;       // setup: publish this rank's edge planes of state `step`
   Coefs c;
+  Watch watch;         // a neighbour that never pushes ends the step (runtime.cu), no trap
 };
 
 __global__ void __launch_bounds__(kEdgeThreads) k_diffusion_slab_edges(const EdgeArgs a) {
   extern __shared__ __align__(16) float sm[];
+  __shared__ int s_dead;  // some thread gave up waiting (CTA-uniform after the barrier)
   const int nz = a.nz, nz4 = nz >> 2, ny = a.ny, nx = a.nx, TJ = a.TJ;
   const int n2 = (nz + 1) / 2;  // words per row: two values each
   const int side = blockIdx.y;  // 0: plane 0 (halo from rank-1), 1: plane nx-1 (halo from rank+1)
@@ -75,6 +81,8 @@ __global__ void __launch_bounds__(kEdgeThreads) k_diffusion_slab_edges(const Edg
   }
   float* halo = sm;            // [TJ][nz] the neighbour's plane of state `step`, rows j0..
   float* res = sm + TJ * nz;   // [TJ][nz] this CTA's new edge rows (state step+1)
+  if (tid == 0) s_dead = 0;
+  __syncthreads();
   if (in) {
     const unsigned int want = static_cast<unsigned int>(a.step + 1);
     const unsigned long long t0 = globaltimer_ns();
@@ -82,10 +90,15 @@ __global__ void __launch_bounds__(kEdgeThreads) k_diffusion_slab_edges(const Edg
       const int r = w / n2, t = w - r * n2, k = 2 * t;
       const uint4* src = in + word(a.step & 1, j0 + r, t);
       uint4 v = ld_relaxed_sys_b128(src);  // written by a peer GPU: system scope
+      bool dead = false;
       while (v.y != want || v.w != want) {  // the neighbour's row (both halves) is not there yet
-        if (globaltimer_ns() - t0 > 4000000000ull) __trap();  // a dead peer fails the step instead of hanging
+        if ((dead = poll_expired(a.watch, t0, kFaultSlabEdges))) break;  // a dead peer: give up, no hang
         __nanosleep(64);
         v = ld_relaxed_sys_b128(src);
+      }
+      if (dead) {
+        s_dead = 1;
+        break;
       }
       float* d = halo + r * nz + k;
       d[0] = __uint_as_float(v.x);
@@ -93,6 +106,7 @@ __global__ void __launch_bounds__(kEdgeThreads) k_diffusion_slab_edges(const Edg
     }
   }
   __syncthreads();
+  if (s_dead) return;  // uniform: no edge planes, nothing pushed (b2_fault_status reports it)
   const float* fo = a.f + static_cast<size_t>(side ? nx - 2 : 1) * plane;  // the in-slab i neighbour
   for (int u = tid; u < rows * nz4; u += blockDim.x) {
     const int r = u / nz4, c4 = u - r * nz4, j = j0 + r;
@@ -132,6 +146,7 @@ struct Xchg2Args {
   uint4* out_lo;  // the neighbours' sides fed by me (null: no neighbour)
   uint4* out_hi;
   int xchg, phase;
+  Watch watch;
 };
 
 __global__ void __launch_bounds__(kEdgeThreads) k_diffusion_slab_halo2(const Xchg2Args a) {
@@ -164,7 +179,7 @@ __global__ void __launch_bounds__(kEdgeThreads) k_diffusion_slab_halo2(const Xch
     const uint4* src = in + word(p, j0 + r, t);
     uint4 v = ld_relaxed_sys_b128(src);
     while (v.y != tag || v.w != tag) {
-      if (globaltimer_ns() - t0 > 4000000000ull) __trap();  // a dead peer fails the run instead of hanging
+      if (poll_expired(a.watch, t0, kFaultHalo2)) return;  // a dead peer: give up (watchdog), no hang
       __nanosleep(64);
       v = ld_relaxed_sys_b128(src);
     }
@@ -209,7 +224,8 @@ int b2_diffusion3d_slab_edges(int nx_local, int ny, int nz, float dx, float dy, 
              static_cast<uint4*>(out_hi),
              step,
              push_only,
-             make_coefs(dx, dy, dz, dt, kappa)};
+             make_coefs(dx, dy, dz, dt, kappa),
+             make_watch()};
   const dim3 grid((ny + TJ - 1) / TJ, 2);
   k_diffusion_slab_edges<<<grid, kEdgeThreads, push_only ? 0 : smem, as_stream(stream)>>>(a);
   return launch_status();
@@ -240,7 +256,8 @@ int b2_diffusion3d_slab_halo2(int nx_ext, int ny, int nz, int lo_h, int nx_local
               static_cast<uint4*>(out_lo),
               static_cast<uint4*>(out_hi),
               xchg,
-              phase};
+              phase,
+              make_watch()};
   k_diffusion_slab_halo2<<<dim3((ny + TJ - 1) / TJ, 2), kEdgeThreads, 0, as_stream(stream)>>>(a);
   return launch_status();
 }

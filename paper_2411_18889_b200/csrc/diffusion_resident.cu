@@ -35,7 +35,8 @@ namespace b2 {
 //
 // A producer cannot lap a consumer: exporting step s+2's faces needs the
 // consumer's step s+1 faces, which the consumer exports only after it pulled
-// step s+1's -- so two mailbox parities suffice. Same arithmetic and clamps as
+// step s+1's -- so two mailbox parities suffice. A face that never arrives ends the run
+// through the watchdog (poll_expired, runtime.cu). Same arithmetic and clamps as
 // k_diffusion_direct: bit-identical to single steps.
 struct ResArgs {
   float* f;
@@ -46,6 +47,7 @@ struct ResArgs {
   uint4* mbox;   // [brick][face 0..3][parity][face_cap] 16-byte words, zeroed before launch
   int face_cap;  // words per face: max(BI, BJ) rows x ceil(nz / 3)
   Coefs c;
+  Watch watch;  // a face that never arrives ends the run (runtime.cu), no trap
 #ifdef B2_RESIDENT_TRACE
   unsigned long long* trace;  // [brick][step][4] globaltimer stamps (scripts/trace_resident.cu)
 #endif
@@ -63,8 +65,10 @@ constexpr int kResidentUnits = 6;  // max halo words per thread per step
 
 __global__ void __launch_bounds__(kResidentThreads, 1) k_diffusion_resident(const ResArgs a) {
   extern __shared__ __align__(16) float sm[];
+  __shared__ int s_dead;  // some thread gave up waiting for a face (CTA-uniform after a barrier)
   const int nz = a.nz, nz4 = nz >> 2, ny = a.ny, nx = a.nx;
   const int BJ = a.BJ, nbj = a.nbj;
+  if (threadIdx.x == 0) s_dead = 0;
   const int b = blockIdx.x;
   const int i0 = (b / nbj) * a.BI, j0 = (b % nbj) * BJ;
   const int PI = min(a.BI, nx - i0), PJ = min(BJ, ny - j0);  // planes / rows owned
@@ -192,12 +196,17 @@ __global__ void __launch_bounds__(kResidentThreads, 1) k_diffusion_resident(cons
             v[w] = ld_relaxed_b128(mb + pull_src[w]);  // not there yet: poll again
           }
         }
-        // A neighbour never arrived: fail loudly instead of hanging the GPU. (A poll
-        // back-off of 64-1000 ns was measured slower: the lines are not contended.)
-        if (todo && globaltimer_ns() - t0 > 4000000000ull) __trap();
+        // A neighbour never arrived: give up instead of hanging the GPU (the watchdog
+        // records it; b2_fault_status reports it). (A poll back-off of 64-1000 ns was
+        // measured slower: the lines are not contended.)
+        if (todo && poll_expired(a.watch, t0, kFaultResident)) {
+          s_dead = 1;
+          break;
+        }
       }
     }
     __syncthreads();
+    if (s_dead) return;  // uniform: f / fn left as they were
     B2_TRACE(1);
     // ---- march this thread's column: cur (state s) -> nxt (state s+1); smem only ----
     // (Computing the brick's shell first and exporting it before the interior was
@@ -261,7 +270,7 @@ struct ResPlan {
   size_t smem = 0;
 };
 
-static bool plan_resident(int nx, int ny, int nz, ResPlan& p) {
+static bool resident_plan_for(int nx, int ny, int nz, ResPlan& p) {
   if (nz % 4 != 0 || nz / 4 > kResidentThreads) return false;
   const int nz4 = nz / 4;
   const DeviceInfo& di = device_info();
@@ -290,32 +299,71 @@ static bool plan_resident(int nx, int ny, int nz, ResPlan& p) {
   return p.BI > 0;
 }
 
-// Per-device mailbox for k_diffusion_resident, grown on demand. Launches on one
-// device are chained through an event (each waits for the previous one to
-// finish with the mailbox), so concurrent runs on different streams stay safe.
+// Per-device mailbox for k_diffusion_resident, sized by plan_resident (b2_diffusion3d_plan:
+// allocation and the wait for earlier users happen there, never in the stream-ordered
+// run). Launches on one device are chained through an event (each waits for the
+// previous one to finish with the mailbox), so concurrent runs on different streams
+// stay safe.
 struct Mailbox {
   void* ptr = nullptr;
   size_t bytes = 0;
   cudaEvent_t done = nullptr;
   bool used = false;
 };
+static std::mutex g_mbox_mu;
+static Mailbox g_boxes[64];
 
-bool launch_resident(int nx, int ny, int nz, const Coefs& c, float* f, float* fn, int nsteps,
-                            cudaStream_t s) {
+static size_t resident_mailbox_bytes(const ResPlan& p, int nz) {
+  const int face_cap = std::max(p.BI, p.BJ) * ((nz + 2) / 3);
+  return static_cast<size_t>(p.nbi) * p.nbj * 4 * 2 * face_cap * sizeof(uint4);
+}
+
+int plan_resident(int nx, int ny, int nz) {
   ResPlan p;
-  if (!plan_resident(nx, ny, nz, p)) return false;
+  if (!resident_plan_for(nx, ny, nz, p)) return B2_OK;  // not a resident shape: nothing to set up
+  const size_t bytes = resident_mailbox_bytes(p, nz);
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(g_mbox_mu);
+  Mailbox& mb = g_boxes[dev];
+  cudaError_t e;
+  if (!mb.done && (e = cudaEventCreateWithFlags(&mb.done, cudaEventDisableTiming)) != cudaSuccess) {
+    mb.done = nullptr;
+    return static_cast<int>(e);
+  }
+  if (mb.bytes >= bytes) return B2_OK;
+  if (mb.ptr) {
+    cudaEventSynchronize(mb.done);  // the last run that used the old mailbox is done with it
+    cudaFree(mb.ptr);
+  }
+  mb.ptr = nullptr;
+  mb.bytes = 0;
+  mb.used = false;
+  if ((e = cudaMalloc(&mb.ptr, bytes)) != cudaSuccess) {
+    cudaGetLastError();
+    mb.ptr = nullptr;
+    return static_cast<int>(e);
+  }
+  mb.bytes = bytes;
+  return B2_OK;
+}
+
+bool launch_resident(int nx, int ny, int nz, const Coefs& c, float* f, float* fn, int nsteps, cudaStream_t s) {
+  ResPlan p;
+  if (!resident_plan_for(nx, ny, nz, p)) return false;
   cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
   if (cudaStreamIsCapturing(s, &cap) != cudaSuccess || cap != cudaStreamCaptureStatusNone) {
     cudaGetLastError();
     return false;  // the event chain below is not capturable; per-step path instead
   }
   const int nbricks = p.nbi * p.nbj;
-  static std::mutex mu;
-  static Mailbox boxes[64];
   allow_max_dynamic_smem(reinterpret_cast<const void*>(k_diffusion_resident));
   int dev = 0;
   cudaGetDevice(&dev);
-  std::lock_guard<std::mutex> lk(mu);
+  std::lock_guard<std::mutex> lk(g_mbox_mu);
+  Mailbox& mb = g_boxes[dev];
+  const size_t bytes = resident_mailbox_bytes(p, nz);
+  if (!mb.ptr || mb.bytes < bytes) return false;  // not planned for this shape (b2_diffusion3d_plan)
   int per_sm = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_diffusion_resident, kResidentThreads, p.smem) !=
           cudaSuccess ||
@@ -324,28 +372,9 @@ bool launch_resident(int nx, int ny, int nz, const Coefs& c, float* f, float* fn
     return false;
   }
   const int face_cap = std::max(p.BI, p.BJ) * ((nz + 2) / 3);
-  const size_t bytes = static_cast<size_t>(nbricks) * 4 * 2 * face_cap * sizeof(uint4);
-  Mailbox& mb = boxes[dev];
-  if (!mb.done && cudaEventCreateWithFlags(&mb.done, cudaEventDisableTiming) != cudaSuccess) {
-    cudaGetLastError();
-    return false;
-  }
-  if (mb.bytes < bytes) {
-    if (mb.ptr) {
-      cudaEventSynchronize(mb.done);
-      cudaFree(mb.ptr);
-    }
-    mb.ptr = nullptr;
-    mb.bytes = 0;
-    if (cudaMalloc(&mb.ptr, bytes) != cudaSuccess) {
-      cudaGetLastError();
-      return false;
-    }
-    mb.bytes = bytes;
-  }
   if (mb.used) cudaStreamWaitEvent(s, mb.done, 0);
   cudaMemsetAsync(mb.ptr, 0, bytes, s);  // no stale tags
-  ResArgs a{f, fn, nx, ny, nz, nsteps, p.BI, p.BJ, p.nbj, static_cast<uint4*>(mb.ptr), face_cap, c};
+  ResArgs a{f, fn, nx, ny, nz, nsteps, p.BI, p.BJ, p.nbj, static_cast<uint4*>(mb.ptr), face_cap, c, make_watch()};
   void* args[] = {&a};
   if (cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(k_diffusion_resident), nbricks, kResidentThreads,
                                   args, p.smem, s) != cudaSuccess) {

@@ -332,41 +332,51 @@ bool plan_tb2(int nx, int ny, int nz, TB2Plan& best) {
   return true;
 }
 
-// On the first run of a grid shape, time the model's best few plans on the caller's own
-// buffers (f read, fn written: fn is scratch until the run writes it) and keep the
-// fastest for that shape and device. Every plan gives the same bits, so the choice only
-// moves time. Host-synchronising, hence skipped while the stream is being captured;
+// Tuned plans per (nx, ny, nz, device). b2_diffusion3d_plan times the model's best few
+// plans on the caller's own buffers (f read, fn written: fn is scratch until the run
+// writes it) and keeps the fastest. Every plan gives the same bits, so the choice only
+// moves time. The stream-ordered run only looks the plan up (no timing, no host
+// synchronisation) and takes the model's pick for shapes nobody planned.
+static std::mutex g_tb2_mu;
+static std::map<std::tuple<int, int, int, int>, TB2Plan> g_tb2_cache;
+
+bool plan_tb2_lookup(int nx, int ny, int nz, TB2Plan& best) {
+  if (!plan_tb2(nx, ny, nz, best)) return false;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(g_tb2_mu);
+  auto it = g_tb2_cache.find(std::make_tuple(nx, ny, nz, dev));
+  if (it != g_tb2_cache.end()) best = it->second;
+  return true;
+}
+
+// Host-synchronising, hence skipped while the stream is being captured;
 // SOLOMON_DIFF_AUTOTUNE=0 keeps the model's pick.
-bool plan_tb2_tuned(int nx, int ny, int nz, const Coefs& c, const float* f, float* fn, cudaStream_t s,
-                    TB2Plan& best) {
+int plan_tb2_tune(int nx, int ny, int nz, const Coefs& c, const float* f, float* fn, cudaStream_t s) {
   static const int autotune = env_int("SOLOMON_DIFF_AUTOTUNE", 1);
-  static std::mutex mu;
-  static std::map<std::tuple<int, int, int, int>, TB2Plan> cache;
   int dev = 0;
   cudaGetDevice(&dev);
   const auto key = std::make_tuple(nx, ny, nz, dev);
   {
-    std::lock_guard<std::mutex> lk(mu);
-    auto it = cache.find(key);
-    if (it != cache.end()) {
-      best = it->second;
-      return true;
-    }
+    std::lock_guard<std::mutex> lk(g_tb2_mu);
+    if (g_tb2_cache.count(key)) return B2_OK;
   }
   const auto cand = tb2_candidates(nx, ny, nz);
-  if (cand.empty()) return false;
-  best = cand.front().second;
+  if (cand.empty()) return B2_OK;
+  TB2Plan best = cand.front().second;
   cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
   if (!autotune || cand.size() == 1 || cudaStreamIsCapturing(s, &cap) != cudaSuccess ||
       cap != cudaStreamCaptureStatusNone) {
     cudaGetLastError();
-    return true;  // model pick, not cached: a later uncaptured call may still tune
+    return B2_OK;  // model pick, not cached: a later uncaptured plan call may still tune
   }
   constexpr int kCandidates = 4;
   cudaEvent_t ev[2];
-  if (cudaEventCreate(&ev[0]) != cudaSuccess || cudaEventCreate(&ev[1]) != cudaSuccess) {
-    cudaGetLastError();
-    return true;
+  cudaError_t e;
+  if ((e = cudaEventCreate(&ev[0])) != cudaSuccess) return static_cast<int>(e);
+  if ((e = cudaEventCreate(&ev[1])) != cudaSuccess) {
+    cudaEventDestroy(ev[0]);
+    return static_cast<int>(e);
   }
   float best_ms = 1e30f;
   for (size_t i = 0; i < cand.size() && i < static_cast<size_t>(kCandidates); ++i) {
@@ -388,9 +398,9 @@ bool plan_tb2_tuned(int nx, int ny, int nz, const Coefs& c, const float* f, floa
   }
   cudaEventDestroy(ev[0]);
   cudaEventDestroy(ev[1]);
-  std::lock_guard<std::mutex> lk(mu);
-  cache[key] = best;
-  return true;
+  std::lock_guard<std::mutex> lk(g_tb2_mu);
+  g_tb2_cache[key] = best;
+  return launch_status();
 }
 
 template <int S1, int S2>

@@ -25,57 +25,48 @@ namespace b2 {
 
 static thread_local int g_last_error = B2_OK;
 
-const DeviceInfo& device_info() {
-  static DeviceInfo infos[64];
-  static bool ready[64] = {};
-  static std::mutex mu;
-  int dev = 0;
-  cudaGetDevice(&dev);
-  std::lock_guard<std::mutex> lk(mu);
-  if (!ready[dev]) {
-    cudaDeviceGetAttribute(&infos[dev].sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaDeviceGetAttribute(&infos[dev].smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-    ready[dev] = true;
-  }
-  return infos[dev];
-}
-
-void allow_max_dynamic_smem(const void* fn) {
-  static std::mutex mu;
-  static std::vector<std::pair<int, const void*>> done;
-  int dev = 0;
-  cudaGetDevice(&dev);
-  std::lock_guard<std::mutex> lk(mu);
-  for (const auto& d : done)
-    if (d.first == dev && d.second == fn) return;
-  cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, device_info().smem_optin);
-  done.emplace_back(dev, fn);
-}
-
-// Per-device staging arena for host-pointer calls (grown on demand, never shrunk).
+// Per-device staging arena for host-pointer calls (grown on demand, never shrunk),
+// one lock per device: concurrent drop-in calls on different GPUs do not serialise.
+// The arena stream is a BLOCKING stream: it is ordered after work the caller queued
+// on the legacy default stream (torch's default stream) and vice versa, like the
+// reference's synchronous present(f, fn) call (listing_diffusion.c:10).
 struct Arena {
   void* ptr = nullptr;
   size_t bytes = 0;
   cudaStream_t stream = nullptr;
 };
 
-static std::mutex g_arena_mu;
-static Arena g_arena[64];
+constexpr int kMaxDev = 64;
+static std::mutex g_arena_mu[kMaxDev];
+static Arena g_arena[kMaxDev];
 
-static void* arena_get(size_t bytes, cudaStream_t* s) {
+static int current_device() {
   int dev = 0;
   cudaGetDevice(&dev);
+  return dev;
+}
+
+// 0 on success, else the cudaError_t of the failed stream creation / allocation.
+static int arena_get(int dev, size_t bytes, void** out, cudaStream_t* s) {
   Arena& a = g_arena[dev];
-  if (!a.stream) cudaStreamCreateWithFlags(&a.stream, cudaStreamNonBlocking);
+  cudaError_t e;
+  if (!a.stream && (e = cudaStreamCreateWithFlags(&a.stream, cudaStreamDefault)) != cudaSuccess) {
+    a.stream = nullptr;
+    return static_cast<int>(e);
+  }
   if (a.bytes < bytes) {
     if (a.ptr) cudaFree(a.ptr);
     a.ptr = nullptr;
     a.bytes = 0;
-    if (cudaMalloc(&a.ptr, bytes) != cudaSuccess) return nullptr;
+    if ((e = cudaMalloc(&a.ptr, bytes)) != cudaSuccess) {
+      cudaGetLastError();
+      return static_cast<int>(e);
+    }
     a.bytes = bytes;
   }
   *s = a.stream;
-  return a.ptr;
+  *out = a.ptr;
+  return B2_OK;
 }
 
 // Copy-in / copy-out streams and per-chunk events for the pipelined host path.
@@ -86,9 +77,7 @@ struct Pipe {
 };
 static Pipe g_pipe[64];
 
-static Pipe& pipe_get() {
-  int dev = 0;
-  cudaGetDevice(&dev);
+static Pipe& pipe_get(int dev) {
   Pipe& p = g_pipe[dev];
   if (!p.in) {
     cudaStreamCreateWithFlags(&p.in, cudaStreamNonBlocking);
@@ -123,14 +112,16 @@ static int calc_acc_dropin(int Ni, void* ipos, void* iacc, int Nj, void* jpos, f
   if (Ni == 0) return B2_OK;
   const bool dev = is_device_ptr(ipos) && is_device_ptr(iacc) && (Nj == 0 || is_device_ptr(jpos));
   const size_t ws = b2_calc_acc_workspace_bytes(Ni, Nj, flags);
-  std::lock_guard<std::mutex> lk(g_arena_mu);
+  const int d = current_device();
+  std::lock_guard<std::mutex> lk(g_arena_mu[d]);
+  cudaStream_t s;
+  int rc;
   if (dev) {
-    cudaStream_t s;
-    void* w = ws ? arena_get(ws, &s) : (arena_get(256, &s));
-    if (!w) return B2_ENOMEM;
-    int rc = b2_calc_acc(Ni, static_cast<float*>(ipos), static_cast<float*>(iacc), Nj, static_cast<float*>(jpos), eps,
-                         flags, w, ws, s);
-    if (rc) return rc;
+    void* w = nullptr;
+    if ((rc = arena_get(d, ws ? ws : 256, &w, &s))) return rc;
+    if ((rc = b2_calc_acc(Ni, static_cast<float*>(ipos), static_cast<float*>(iacc), Nj, static_cast<float*>(jpos),
+                          eps, flags, w, ws, s)))
+      return rc;
     cudaError_t e = cudaStreamSynchronize(s);
     return e == cudaSuccess ? B2_OK : static_cast<int>(e);
   }
@@ -138,17 +129,16 @@ static int calc_acc_dropin(int Ni, void* ipos, void* iacc, int Nj, void* jpos, f
   const size_t bj = align_up(sizeof(float4) * static_cast<size_t>(Nj));
   const bool same = ipos == jpos && Ni == Nj;
   const size_t total = bi /*ipos*/ + bi /*iacc*/ + (same ? 0 : bj) + align_up(ws);
-  cudaStream_t s;
-  char* base = static_cast<char*>(arena_get(total, &s));
-  if (!base) return B2_ENOMEM;
+  void* basev = nullptr;
+  if ((rc = arena_get(d, total, &basev, &s))) return rc;
+  char* base = static_cast<char*>(basev);
   float* d_i = reinterpret_cast<float*>(base);
   float* d_a = reinterpret_cast<float*>(base + bi);
   float* d_j = same ? d_i : reinterpret_cast<float*>(base + 2 * bi);
   void* d_w = base + 2 * bi + (same ? 0 : bj);
   cudaMemcpyAsync(d_i, ipos, sizeof(float4) * static_cast<size_t>(Ni), cudaMemcpyDefault, s);
   if (!same && Nj) cudaMemcpyAsync(d_j, jpos, sizeof(float4) * static_cast<size_t>(Nj), cudaMemcpyDefault, s);
-  int rc = b2_calc_acc(Ni, d_i, d_a, Nj, d_j, eps, flags, d_w, ws, s);
-  if (rc) return rc;
+  if ((rc = b2_calc_acc(Ni, d_i, d_a, Nj, d_j, eps, flags, d_w, ws, s))) return rc;
   cudaMemcpyAsync(iacc, d_a, sizeof(float4) * static_cast<size_t>(Ni), cudaMemcpyDefault, s);
   cudaError_t e = cudaStreamSynchronize(s);
   return e == cudaSuccess ? B2_OK : static_cast<int>(e);
@@ -158,26 +148,29 @@ static int diffusion_dropin(int nx, int ny, int nz, float dx, float dy, float dz
                             const float* f, float* fn) {
   if (nx <= 0 || ny <= 0 || nz <= 0 || !f || !fn || f == fn) return B2_EINVAL;
   const size_t n = static_cast<size_t>(nx) * ny * nz;
-  std::lock_guard<std::mutex> lk(g_arena_mu);
+  const int d = current_device();
+  std::lock_guard<std::mutex> lk(g_arena_mu[d]);
+  cudaStream_t s;
+  void* basev = nullptr;
+  int rc;
   if (is_device_ptr(f) && is_device_ptr(fn)) {
-    cudaStream_t s;
-    if (!arena_get(256, &s)) return B2_ENOMEM;
-    int rc = b2_diffusion3d(nx, ny, nz, dx, dy, dz, dt, kappa, f, fn, s);
-    if (rc) return rc;
+    if ((rc = arena_get(d, 256, &basev, &s))) return rc;
+    // synchronous call: time the step's tile plans once per shape (b2_diffusion3d_plan)
+    if ((rc = b2_diffusion3d_plan(nx, ny, nz, dx, dy, dz, dt, kappa, f, fn, 1, s))) return rc;
+    if ((rc = b2_diffusion3d(nx, ny, nz, dx, dy, dz, dt, kappa, f, fn, s))) return rc;
     cudaError_t e = cudaStreamSynchronize(s);
     return e == cudaSuccess ? B2_OK : static_cast<int>(e);
   }
   const size_t b = align_up(n * sizeof(float));
-  cudaStream_t s;
-  char* base = static_cast<char*>(arena_get(2 * b, &s));
-  if (!base) return B2_ENOMEM;
+  if ((rc = arena_get(d, 2 * b, &basev, &s))) return rc;
+  char* base = static_cast<char*>(basev);
   float* d_f = reinterpret_cast<float*>(base);
   float* d_fn = reinterpret_cast<float*>(base + b);
   // Host buffers: pipeline the step over plane chunks so the H2D copy of chunk
   // c+1, the stencil on chunk c and the D2H copy of chunk c-1 overlap (two copy
   // engines + SMs). Output planes [lo, hi) need input planes lo-1..hi, i.e. the
   // chunk itself and the first plane of the next one.
-  Pipe& P = pipe_get();
+  Pipe& P = pipe_get(d);
   const size_t plane = static_cast<size_t>(ny) * nz;
   const int K = std::max(1, std::min(kMaxChunks, nx / 16));
   auto lo_of = [&](int c) { return static_cast<int>(static_cast<long long>(c) * nx / K); };
@@ -189,9 +182,9 @@ static int diffusion_dropin(int nx, int ny, int nz, float dx, float dy, float dz
   for (int c = 0; c < K; ++c) {
     cudaStreamWaitEvent(s, P.ev_in[c], 0);
     if (c + 1 < K) cudaStreamWaitEvent(s, P.ev_in[c + 1], 0);
-    int rc = b2_diffusion3d_slab(nx, ny, nz, dx, dy, dz, dt, kappa, d_f, nullptr, nullptr, d_fn, lo_of(c),
-                                 lo_of(c + 1), s);
-    if (rc) return rc;
+    if ((rc = b2_diffusion3d_slab(nx, ny, nz, dx, dy, dz, dt, kappa, d_f, nullptr, nullptr, d_fn, lo_of(c),
+                                  lo_of(c + 1), s)))
+      return rc;
     cudaEventRecord(P.ev_comp[c], s);
   }
   for (int c = 0; c < K; ++c) {
@@ -226,19 +219,16 @@ void diffusion3d(int nx, int ny, int nz, float dx, float dy, float dz, float dt,
   report("diffusion3d", diffusion_dropin(nx, ny, nz, dx, dy, dz, dt, kappa, f, fn));
 }
 
-int b2_last_error(void) { return g_last_error; }
-
-const char* b2_error_string(int code) {
-  switch (code) {
-    case B2_OK: return "ok";
-    case B2_EINVAL: return "invalid argument";
-    case B2_EALIGN: return "pointer not 16-byte aligned";
-    case B2_ESPACE: return "workspace too small";
-    case B2_ENOMEM: return "out of device memory";
-    default: return code > 0 ? cudaGetErrorString(static_cast<cudaError_t>(code)) : "unknown error";
-  }
+void calc_acc_exact(const int Ni, solomon_float4* ipos, solomon_float4* iacc, const int Nj, solomon_float4* jpos,
+                    const float eps) {
+  report("calc_acc_exact", calc_acc_dropin(Ni, ipos, iacc, Nj, jpos, eps, B2_EXACT));
 }
 
-const char* b2_version(void) { return "solomon_b200 0.1.0 (sm_100a)"; }
+void calc_acc_potential_exact(const int Ni, solomon_float4* ipos, solomon_float4* iacc, const int Nj,
+                              solomon_float4* jpos, const float eps) {
+  report("calc_acc_potential_exact", calc_acc_dropin(Ni, ipos, iacc, Nj, jpos, eps, B2_POTENTIAL | B2_EXACT));
+}
+
+int b2_last_error(void) { return g_last_error; }
 
 }  // extern "C"

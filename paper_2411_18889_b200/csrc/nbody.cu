@@ -138,11 +138,12 @@ __global__ void __launch_bounds__(BLOCK, MINB)
   const int j1 = min(j0 + jchunk, Nj);
   const int ntiles = (j1 - j0 + BLOCK - 1) / BLOCK;
 
-  // Padding j (beyond j1) gets m = 0 at the origin: contributes exactly 0
-  // whenever the reference itself is finite (eps > 0).
+  // Padding j (beyond j1) gets m = 0 far away (1e18 on every axis): r2 ~ 3e36 stays
+  // finite, w = rsqrt(r2)^3 * 0 = 0, so it adds exactly +0 -- also for eps = 0 and an
+  // i-particle at the origin, where a padding j AT the origin would give inf * 0 = NaN.
   auto fetch = [&](int t) -> float4 {
     const int j = j0 + t * BLOCK + tid;
-    return j < j1 ? __ldg(jpos + j) : make_float4(0.f, 0.f, 0.f, 0.f);
+    return j < j1 ? __ldg(jpos + j) : make_float4(1e18f, 1e18f, 1e18f, 0.f);
   };
   auto stash = [&](int buf, float4 pj) {
     if (DUP == 1) {

@@ -24,7 +24,8 @@ namespace b2 {
 // self-validating 16-byte words {x, y, z, step tag} (masses never change, so
 // the tag takes .w's place; each CTA keeps the masses it gathers in registers):
 // a .b128 store/load is single-copy atomic, so consumers poll the data itself
-// -- no grid barrier, no fence. Two tag parities suffice: a CTA publishes step
+// -- no grid barrier, no fence. A word that never arrives ends the run through
+// the watchdog (poll_expired, runtime.cu) instead of hanging. Two tag parities suffice: a CTA publishes step
 // s+2's positions only after gathering every CTA's step s+1 positions, which
 // each CTA publishes only after it finished reading step s's.
 //
@@ -59,6 +60,7 @@ struct SmallArgs {
   int nsteps, flags;  // B2_POTENTIAL | B2_INIT_ACC
   int chunk, nch;
   int I;  // i-particles per CTA: 4 * ceil(n / (4 * SMs)) <= 32, so the grid spans every SM
+  Watch watch;  // a position word that never arrives ends the run (runtime.cu), no trap
 #ifdef B2_SMALL_TRACE
   unsigned long long* trace;  // [cta][step][4] globaltimer stamps (scripts/trace_small.cu)
 #endif
@@ -74,7 +76,9 @@ struct SmallArgs {
 template <bool POT>
 __global__ void __launch_bounds__(kSmallThreads, 1) k_leapfrog_small(const SmallArgs a) {
   extern __shared__ float4 sm4[];
+  __shared__ int s_dead;  // some thread of this CTA gave up waiting (CTA-uniform after a barrier)
   const int n = a.n, tid = threadIdx.x;
+  if (tid == 0) s_dead = 0;
   float4* P = sm4;                   // positions {x, y, z, m} of the current state, j at j + j / chunk
   const int IB = a.I;                // i-particles per CTA (the last CTA may own fewer)
   float4* part = sm4 + n + a.nch;    // [nch][IB] chunk partials of this CTA's i
@@ -206,10 +210,14 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_leapfrog_small(const Small
             w[k] = ld_relaxed_b128(src + j);
           }
         }
-        if (todo && globaltimer_ns() - t0 > 4000000000ull) __trap();  // a CTA never published: fail, don't hang
+        if (todo && poll_expired(a.watch, t0, kFaultLeapfrogSmall)) {  // a CTA never published: give up
+          s_dead = 1;
+          break;
+        }
       }
     }
     __syncthreads();
+    return s_dead == 0;  // false: leave without writing pos / vel / acc (b2_fault_status reports it)
   };
 
   const float h = a.h;
@@ -220,7 +228,7 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_leapfrog_small(const Small
     for (int st = 0; st < a.nsteps; ++st) {
       B2_STRACE(0);
       __syncthreads();  // everyone is done reading P
-      gather(st + 1);
+      if (!gather(st + 1)) return;
       B2_STRACE(1);
       force();
       B2_STRACE(2);
@@ -278,7 +286,7 @@ bool launch_leapfrog_small(int n, float4* pos, float4* vel, float4* acc, float e
     return false;
   }
   SmallArgs args{n, pos, vel, acc, pub, eps * eps, dt, 0.5f * dt, nsteps, flags & (B2_POTENTIAL | B2_INIT_ACC),
-                 chunk_size(n, flags & B2_POTENTIAL), nch, I};
+                 chunk_size(n, flags & B2_POTENTIAL), nch, I, make_watch()};
   void* argv[] = {&args};
   if (cudaLaunchCooperativeKernel(fn, ctas, kSmallThreads, argv, smem, s) != cudaSuccess) {
     cudaGetLastError();

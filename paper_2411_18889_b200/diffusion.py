@@ -16,7 +16,25 @@ from dataclasses import dataclass, field
 
 import torch
 
-from ._lib import check, load, on_device, require_cuda, stream_handle
+from ._lib import check, check_fault, load, on_device, require_cuda, stream_handle
+
+_planned: set[tuple] = set()  # (shape, device, nsteps class) already passed to b2_diffusion3d_plan
+
+
+def plan(f: torch.Tensor, fn: torch.Tensor, dx: float, dy: float, dz: float, dt: float, kappa: float,
+         nsteps: int = 1) -> None:
+    """Set-up call (b2_diffusion3d_plan): time the tile plans of this grid shape on ``f`` (read)
+    and ``fn`` (written: scratch) and, for ``nsteps >= 2``, of the multi-step kernels, and size
+    the resident path's mailbox. Host-synchronising, once per shape and device; the step and
+    run calls then stay stream-ordered. Plans change time, never bits."""
+    nx, ny, nz = f.shape
+    key = (nx, ny, nz, f.device, min(int(nsteps), 2))
+    if key in _planned:
+        return
+    with on_device(f.device):
+        check(load().b2_diffusion3d_plan(nx, ny, nz, dx, dy, dz, dt, kappa, f.data_ptr(), fn.data_ptr(), int(nsteps),
+                                         stream_handle(f.device)), "diffusion3d_plan")
+    _planned.add(key)
 
 
 def _grid(t: torch.Tensor, n: int, name: str) -> None:
@@ -46,12 +64,17 @@ def diffusion3d(nx: int, ny: int, nz: int, dx: float, dy: float, dz: float, dt: 
     """One explicit step ``fn = f + kappa dt lap(f)`` with clamped boundaries (listing_diffusion.c:5-25).
 
     Stream-ordered on the current CUDA stream; bit-identical to the reference's -O3 build.
+    The first call for a grid shape on a device plans its tiles (``plan``: host-synchronising
+    once, before the step, writing ``fn``).
     """
     n = nx * ny * nz
     _grid(f, n, "f")
     _grid(fn, n, "fn")
     if f.data_ptr() == fn.data_ptr():
         raise ValueError("f and fn must not alias (restrict, listing_diffusion.c:5)")
+    if (nx, ny, nz, f.device, 1) not in _planned and not torch.cuda.is_current_stream_capturing():
+        plan(f.view(nx, ny, nz) if f.numel() == n else f.flatten()[:n].view(nx, ny, nz),
+             fn.view(nx, ny, nz) if fn.numel() == n else fn.flatten()[:n].view(nx, ny, nz), dx, dy, dz, dt, kappa, 1)
     with on_device(f.device):
         check(load().b2_diffusion3d(nx, ny, nz, dx, dy, dz, dt, kappa, f.data_ptr(), fn.data_ptr(),
                                     stream_handle(f.device)), "diffusion3d")
@@ -98,6 +121,13 @@ class Diffusion3D:
         _grid(self.f, self.f.numel(), "f")
         self._fn = torch.empty_like(self.f)
         self.steps = 0
+        if not torch.cuda.is_current_stream_capturing():
+            plan(self.f, self._fn, self.dx, self.dy, self.dz, self.dt, self.kappa, nsteps=2)
+
+    def synchronize(self) -> None:
+        """Wait for the queued steps; raises SolomonError if a device-side wait gave up
+        (the resident path's bricks exchange faces in the GPU; b2_fault_status)."""
+        check_fault(self.f.device, "Diffusion3D.run")
 
     @property
     def field(self) -> torch.Tensor:

@@ -74,6 +74,12 @@ class CudaSlabKernels:
                    "diffusion3d_slab")
 
 
+    def plan(self, f, fn, nsteps) -> None:
+        """Tile plans for this slab shape (b2_diffusion3d_plan; set-up, host-synchronising)."""
+        from .diffusion import plan
+
+        plan(f, fn, *self.args, nsteps=nsteps)
+
     def run2(self, f, fn) -> bool:
         """Two steps over a (halo-extended) slab; True when the result is in fn."""
         nx, ny, nz = f.shape
@@ -199,16 +205,6 @@ class ShardedLeapfrog:
     @property
     def pos(self) -> torch.Tensor:
         return self._bufs[self._cur][self.plan.lo:self.plan.hi]  # contiguous view: in-place gather source
-
-    def _agree_planes(self, ny: int, nz: int) -> None:
-        """Every rank must hold [*, ny, nz] planes (a halo is one plane). Checked collectively,
-        so a mismatch raises on every rank instead of deadlocking the first exchange."""
-        dev = self.f.device if dist.get_backend(self.group) == "nccl" else torch.device("cpu")
-        t = torch.tensor([ny, nz, -ny, -nz], dtype=torch.int64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX, group=self.group)
-        hy, hz, ly, lz = (int(v) for v in t.tolist())
-        if (hy, hz, -ly, -lz) != (ny, nz, ny, nz):
-            raise ValueError(f"ranks hold different planes: ny in [{-ly}, {hy}], nz in [{-lz}, {hz}]")
 
     # ---- p2p transport -------------------------------------------------------
     def _setup_p2p(self) -> None:
@@ -338,6 +334,11 @@ class ShardedLeapfrog:
     def launches_per_step(self) -> int:
         return 2
 
+    def synchronize(self) -> None:
+        """Wait for this rank's queued steps; raises SolomonError if a device-side wait gave up."""
+        if self.pos_all.is_cuda:
+            _lib.check_fault(self.pos_all.device, "ShardedLeapfrog.step")
+
     # ---- checkpoint / resume (SURVEY.md §5) -----------------------------------
     def state_dict(self) -> dict:
         """This rank's shard. ``opened`` records a pending opening half-kick
@@ -412,6 +413,9 @@ class SlabDiffusion:
         self.is_cuda = self.f.is_cuda
         self.transport = transport
         self.steps_done = 0
+        if self.is_cuda and hasattr(self.k, "plan"):  # set-up: time the tile plans once (writes fn: scratch)
+            self.k.plan(self.f, self.fn, 1)  # step(): the interior planes of the slab
+            self.k.plan(*self._ext, 2)       # run(): two steps per pass over the halo-extended slab
         if transport == "nccl":
             self.halo_lo = torch.empty((ny, nz), dtype=self.f.dtype, device=self.f.device) if self.has_lo else None
             self.halo_hi = torch.empty((ny, nz), dtype=self.f.dtype, device=self.f.device) if self.has_hi else None
@@ -442,10 +446,10 @@ class SlabDiffusion:
         lib = _lib.load()
         self.ctrl = dist.new_group(backend="gloo") if dist.get_backend(self.group) != "gloo" else self.group
         ny, nz = self.f.shape[1:]
-        self._side = int(lib.b2_diffusion3d_mailbox_bytes(ny, nz))
+        self._side_bytes = int(lib.b2_diffusion3d_mailbox_bytes(ny, nz))
         self._side2 = int(lib.b2_diffusion3d_mailbox2_bytes(ny, nz))
         # [per-step: fed by rank-1 | by rank+1][run(): fed by rank-1 | by rank+1]
-        self.mbox = torch.zeros(2 * self._side + 2 * self._side2, dtype=torch.uint8, device=self.f.device)
+        self.mbox = torch.zeros(2 * self._side_bytes + 2 * self._side2, dtype=torch.uint8, device=self.f.device)
         hb = lib.b2_ipc_handle_bytes()
         h = ctypes.create_string_buffer(hb)
         off = ctypes.c_size_t(0)
@@ -473,13 +477,16 @@ class SlabDiffusion:
             raise _lib.SolomonError(f"p2p halo transport unavailable on some rank: {err or 'peer failure'}")
         base = self.mbox.data_ptr()
         self._in_lo = base if self.has_lo else None
-        self._in_hi = base + self._side if self.has_hi else None
-        self._out_lo = self._peer[self.rank - 1][0] + self._side if self.has_lo else None  # its side fed by rank+1
+        self._in_hi = base + self._side_bytes if self.has_hi else None
+        self._out_lo = self._peer[self.rank - 1][0] + self._side_bytes if self.has_lo else None  # its side fed by rank+1
         self._out_hi = self._peer[self.rank + 1][0] if self.has_hi else None              # its side fed by rank-1
-        r2 = 2 * self._side  # run() mailboxes, same layout after the per-step pair
+        r2 = 2 * self._side_bytes  # run() mailboxes, same layout after the per-step pair
         self._in2 = (base + r2 if self.has_lo else None, base + r2 + self._side2 if self.has_hi else None)
         self._out2 = (self._peer[self.rank - 1][0] + r2 + self._side2 if self.has_lo else None,
                       self._peer[self.rank + 1][0] + r2 if self.has_hi else None)
+        self._side = torch.cuda.Stream(device=self.f.device)  # the edge kernel of step()
+        self._state_ready = torch.cuda.Event()  # main stream at the start of a step
+        self._edges_done = torch.cuda.Event()
         self._publish_edges()
 
     def _edges(self, push_only: bool) -> None:
@@ -494,7 +501,7 @@ class SlabDiffusion:
     def _publish_edges(self) -> None:
         """(Re)start the per-step exchange at state steps_done: every per-step mailbox zero, then
         every rank pushes. (run()'s mailboxes keep their monotonic exchange tags.)"""
-        self.mbox[:2 * self._side].zero_()
+        self.mbox[:2 * self._side_bytes].zero_()
         torch.cuda.synchronize(self.f.device)
         dist.barrier(group=self.ctrl)
         self._edges(push_only=True)
@@ -544,9 +551,19 @@ class SlabDiffusion:
 
     def _step_p2p(self) -> None:
         nxl = self.f.shape[0]
+        main = torch.cuda.current_stream(self.f.device)
+        self._state_ready.record(main)  # everything queued so far (previous step, user copies into f)
         if nxl > 2:  # interior planes need no halo
             self.k.slab(self.f, self.fn, None, None, 1, nxl - 1)
-        self._edges(push_only=False)  # edge planes + halo exchange, synchronised on the device
+        # edge planes + halo exchange, synchronised on the device, on a second stream so the
+        # wait for the neighbours' rows overlaps the interior launch (queued first, so its
+        # CTAs take the SMs first; the edge kernel's small CTAs run beside them). Planes 0 and
+        # nxl-1 of fn are the edge kernel's, 1..nxl-2 the interior's: disjoint writes.
+        self._side.wait_event(self._state_ready)
+        with torch.cuda.stream(self._side):
+            self._edges(push_only=False)
+        self._edges_done.record(self._side)
+        main.wait_event(self._edges_done)
 
     def step(self, nsteps: int = 1) -> torch.Tensor:
         for _ in range(nsteps):
@@ -612,6 +629,13 @@ class SlabDiffusion:
     def launches_per_step(self) -> int:
         interior = 1 if self.f.shape[0] > 2 else 0
         return interior + (1 if self.transport == "p2p" else 2)
+
+    def synchronize(self) -> None:
+        """Wait for this rank's queued steps; raises SolomonError if a device-side wait for a
+        neighbour's halo gave up (p2p transport: the peer is dead or stalled past the poll
+        timeout, ``_lib.set_poll_timeout``). The context stays usable; the slab does not."""
+        if self.is_cuda:
+            _lib.check_fault(self.f.device, f"SlabDiffusion (rank {self.rank})")
 
     # ---- checkpoint / resume (SURVEY.md §5) -----------------------------------
     def state_dict(self) -> dict:

@@ -165,6 +165,11 @@ class Leapfrog:
     def kernel_launches_per_step(self) -> int:
         return 2
 
+    def synchronize(self) -> None:
+        """Wait for the queued steps; raises SolomonError if a device-side wait gave up
+        (the persistent small-N path exchanges positions between CTAs in the GPU)."""
+        _lib.check_fault(self.pos.device, "Leapfrog.step")
+
     # ---- checkpoint / resume (SURVEY.md §5) -----------------------------------
     def state_dict(self) -> dict:
         """Positions, velocities (synchronised: every step closes with its half-kick),

@@ -105,14 +105,27 @@ def synchronize() -> None:
     torch.cuda.synchronize()
 
 
+def _refcount(a: np.ndarray) -> int:
+    with _lock:
+        entry = _table.get(_key(a))
+        return entry[2] if entry else 0
+
+
 @contextlib.contextmanager
 def data_access_by_device(copyin=(), copyout=(), copy=(), create=()):
-    """DATA_ACCESS_BY_DEVICE: a structured data region (acc data copyin/copyout/copy/create)."""
-    arrays = list(copyin) + list(copyout) + list(copy) + list(create)
+    """DATA_ACCESS_BY_DEVICE: a structured data region (acc data copyin/copyout/copy/create).
+
+    present_or_* semantics, as OpenACC data regions: an array already present (an
+    enclosing region or MALLOC_ON_DEVICE) only gains a reference -- copy-in happens
+    when its count goes 0 -> 1 and copy-out when it returns 1 -> 0, so a nested
+    region neither overwrites newer device data nor copies out early."""
+    arrays = list({_key(a): a for a in (*copyin, *copyout, *copy, *create)}.values())  # one reference each
+    fresh = [a for a in arrays if _refcount(a) == 0]
+    fresh_keys = {_key(a) for a in fresh}
     malloc_on_device(*arrays)
     try:
-        memcpy_h2d(*copyin, *copy)
+        memcpy_h2d(*[a for a in (*copyin, *copy) if _key(a) in fresh_keys])
         yield
-        memcpy_d2h(*copyout, *copy)
+        memcpy_d2h(*[a for a in (*copyout, *copy) if _refcount(a) == 1])
     finally:
         free_from_device(*arrays)

@@ -25,6 +25,7 @@ const DeviceInfo& device_info() {
 void allow_max_dynamic_smem(const void* fn) {
   cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, device_info().smem_optin);
 }
+Watch make_watch() { return Watch{nullptr, 4000000000ull}; }
 }  // namespace b2
 
 int main(int argc, char** argv) {
@@ -39,7 +40,7 @@ int main(int argc, char** argv) {
   cudaMalloc(&fn, cells * 4);
   cudaMemcpy(f, h.data(), cells * 4, cudaMemcpyHostToDevice);
   ResPlan p;
-  if (!plan_resident(n, n, n, p)) {
+  if (!resident_plan_for(n, n, n, p)) {
     std::printf("no plan\n");
     return 1;
   }
@@ -58,7 +59,7 @@ int main(int argc, char** argv) {
   cudaEventCreate(&e1);
   for (int rep = 0; rep < 3; ++rep) {
     cudaMemset(mbox, 0, mbytes);
-    ResArgs a{f, fn, n, n, n, steps, p.BI, p.BJ, p.nbj, mbox, face_cap, c, trace};
+    ResArgs a{f, fn, n, n, n, steps, p.BI, p.BJ, p.nbj, mbox, face_cap, c, Watch{nullptr, 4000000000ull}, trace};
     void* args[] = {&a};
     cudaEventRecord(e0);
     cudaError_t err = cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(k_diffusion_resident), nb,

@@ -20,6 +20,7 @@ LIB = ROOT / "paper_2411_18889_b200" / "lib" / "libsolomon_b200.so"
 
 def header_functions() -> list[str]:
     text = re.sub(r"/\*.*?\*/", "", HEADER.read_text(), flags=re.S)
+    text = re.sub(r"(?m)^.*\\\n", "", text)  # macro bodies (the C++ float4 overloads)
     names = re.findall(r"^\s*(?:const\s+)?[A-Za-z_][\w\s\*]*?\b([A-Za-z_]\w*)\s*\(", text, flags=re.M)
     return sorted({n for n in names if n not in {"defined", "if", "typedef"}})
 

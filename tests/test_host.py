@@ -93,3 +93,21 @@ def test_residency_requires_mapping():
     if not torch.cuda.is_available():
         with pytest.raises(b2.SolomonError):
             R.malloc_on_device(a)
+
+
+def test_sharded_checkpoint_path_needs_rank_placeholder(tmp_path):
+    """at world size > 1 every rank writing one path would lose shards silently."""
+    import types
+
+    from paper_2411_18889_b200 import checkpoint
+
+    slab = types.SimpleNamespace(rank=1, world=2)
+    with pytest.raises(ValueError, match="rank"):
+        checkpoint._rank_path(tmp_path / "ck.pt", slab)
+    assert checkpoint._rank_path(str(tmp_path / "ck.{rank}.pt"), slab).name == "ck.1.pt"
+    shard = types.SimpleNamespace(plan=types.SimpleNamespace(rank=3, world=4))
+    with pytest.raises(ValueError):
+        checkpoint._rank_path(tmp_path / "ck.pt", shard)
+    assert checkpoint._rank_path(str(tmp_path / "ck.{rank}.pt"), shard).name == "ck.3.pt"
+    single = types.SimpleNamespace()
+    assert checkpoint._rank_path(tmp_path / "ck.pt", single).name == "ck.pt"

@@ -322,6 +322,45 @@ def test_residency_helpers_present_contract(b2, golden):
         R.present(f0)
 
 
+def test_residency_nested_regions_present_or_copy(b2):
+    """a nested DATA_ACCESS_BY_DEVICE on an array already present only adds a
+    reference (OpenACC present_or_copy): no copy-in over newer device data, no early copy-out."""
+    from paper_2411_18889_b200 import residency as R
+
+    a = np.zeros((4, 4), np.float32)
+    with R.data_access_by_device(copy=[a]):
+        R.present(a).fill_(1.0)  # newer device data
+        a[:] = 7.0              # stale host data
+        with R.data_access_by_device(copy=[a]):
+            assert float(R.present(a)[0, 0]) == 1.0  # not overwritten by the inner copy-in
+            R.present(a).add_(1.0)
+        assert float(a[0, 0]) == 7.0  # the inner exit did not copy out
+        assert R.is_present(a)
+    assert float(a[0, 0]) == 2.0  # the outer exit did
+    assert not R.is_present(a)
+
+
+def test_dropin_orders_after_default_stream_work(b2, golden):
+    """device pointers through the synchronous drop-in see work the caller queued on
+    the default stream before the call (a large fill of the output must land BEFORE the result)."""
+    case = "nbody/plummer256"
+    pos = golden[f"{case}/pos"]
+    want = golden[f"{case}/acc"]
+    n = pos.shape[0]
+    big = torch.empty(1 << 28, device="cuda")  # ~1 GiB of queued work ahead of the fill
+    ipos = torch.zeros((n, 4), device="cuda")
+    iacc = torch.empty((n, 4), device="cuda")
+    for _ in range(3):
+        big.fill_(1.0)
+    ipos.copy_(torch.from_numpy(pos))   # queued on the default stream, not yet executed
+    iacc.fill_(float("nan"))
+    P = ctypes.c_void_p
+    b2.load().calc_acc_exact(n, P(ipos.data_ptr()), P(iacc.data_ptr()), n, P(ipos.data_ptr()),
+                             float(golden[f"{case}/eps"]))
+    assert b2.load().b2_last_error() == 0
+    assert bits_equal(iacc.cpu().numpy(), want)
+
+
 @pytest.mark.parametrize("shape,steps", [((40, 37, 128), 2), ((40, 37, 128), 5), ((13, 9, 512), 4),
                                          ((256, 64, 512), 6), ((300, 70, 256), 3), ((66, 130, 1024), 2),
                                          ((5, 3, 2048), 4), ((1, 7, 64), 2), ((2, 1, 512), 4), ((64, 64, 100), 4)])
