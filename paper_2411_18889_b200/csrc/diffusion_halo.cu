@@ -54,7 +54,6 @@ struct EdgeArgs {
 
 __global__ void __launch_bounds__(kEdgeThreads) k_diffusion_slab_edges(const EdgeArgs a) {
   extern __shared__ __align__(16) float sm[];
-  __shared__ int s_dead;  // some thread gave up waiting (CTA-uniform after the barrier)
   const int nz = a.nz, nz4 = nz >> 2, ny = a.ny, nx = a.nx, TJ = a.TJ;
   const int n2 = (nz + 1) / 2;  // words per row: two values each
   const int side = blockIdx.y;  // 0: plane 0 (halo from rank-1), 1: plane nx-1 (halo from rank+1)
@@ -81,8 +80,7 @@ __global__ void __launch_bounds__(kEdgeThreads) k_diffusion_slab_edges(const Edg
   }
   float* halo = sm;            // [TJ][nz] the neighbour's plane of state `step`, rows j0..
   float* res = sm + TJ * nz;   // [TJ][nz] this CTA's new edge rows (state step+1)
-  if (tid == 0) s_dead = 0;
-  __syncthreads();
+  bool gave_up = false;  // this thread's wait expired (voted CTA-wide below)
   if (in) {
     const unsigned int want = static_cast<unsigned int>(a.step + 1);
     const unsigned long long t0 = globaltimer_ns();
@@ -97,7 +95,7 @@ __global__ void __launch_bounds__(kEdgeThreads) k_diffusion_slab_edges(const Edg
         v = ld_relaxed_sys_b128(src);
       }
       if (dead) {
-        s_dead = 1;
+        gave_up = true;
         break;
       }
       float* d = halo + r * nz + k;
@@ -105,8 +103,7 @@ __global__ void __launch_bounds__(kEdgeThreads) k_diffusion_slab_edges(const Edg
       if (k + 1 < nz) d[1] = __uint_as_float(v.z);
     }
   }
-  __syncthreads();
-  if (s_dead) return;  // uniform: no edge planes, nothing pushed (b2_fault_status reports it)
+  if (__syncthreads_or(gave_up)) return;  // uniform: no edge planes, nothing pushed (b2_fault_status reports it)
   const float* fo = a.f + static_cast<size_t>(side ? nx - 2 : 1) * plane;  // the in-slab i neighbour
   for (int u = tid; u < rows * nz4; u += blockDim.x) {
     const int r = u / nz4, c4 = u - r * nz4, j = j0 + r;

@@ -65,10 +65,8 @@ constexpr int kResidentUnits = 6;  // max halo words per thread per step
 
 __global__ void __launch_bounds__(kResidentThreads, 1) k_diffusion_resident(const ResArgs a) {
   extern __shared__ __align__(16) float sm[];
-  __shared__ int s_dead;  // some thread gave up waiting for a face (CTA-uniform after a barrier)
   const int nz = a.nz, nz4 = nz >> 2, ny = a.ny, nx = a.nx;
   const int BJ = a.BJ, nbj = a.nbj;
-  if (threadIdx.x == 0) s_dead = 0;
   const int b = blockIdx.x;
   const int i0 = (b / nbj) * a.BI, j0 = (b % nbj) * BJ;
   const int PI = min(a.BI, nx - i0), PJ = min(BJ, ny - j0);  // planes / rows owned
@@ -157,6 +155,7 @@ __global__ void __launch_bounds__(kResidentThreads, 1) k_diffusion_resident(cons
 
   for (int s = 0; s < a.nsteps; ++s) {
     B2_TRACE(0);
+    bool dead = false;  // this thread gave up waiting for a face
     // ---- pull the halo of state s into cur ----
     if (s == 0) {
       for (int u = tid; u < nu; u += blockDim.x) {
@@ -200,13 +199,13 @@ __global__ void __launch_bounds__(kResidentThreads, 1) k_diffusion_resident(cons
         // records it; b2_fault_status reports it). (A poll back-off of 64-1000 ns was
         // measured slower: the lines are not contended.)
         if (todo && poll_expired(a.watch, t0, kFaultResident)) {
-          s_dead = 1;
+          dead = true;
           break;
         }
       }
     }
-    __syncthreads();
-    if (s_dead) return;  // uniform: f / fn left as they were
+    // barrier + CTA-wide vote (no static shared memory next to the full dynamic allocation)
+    if (__syncthreads_or(dead)) return;  // uniform: f / fn left as they were
     B2_TRACE(1);
     // ---- march this thread's column: cur (state s) -> nxt (state s+1); smem only ----
     // (Computing the brick's shell first and exporting it before the interior was

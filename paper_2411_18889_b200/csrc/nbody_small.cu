@@ -76,9 +76,7 @@ struct SmallArgs {
 template <bool POT>
 __global__ void __launch_bounds__(kSmallThreads, 1) k_leapfrog_small(const SmallArgs a) {
   extern __shared__ float4 sm4[];
-  __shared__ int s_dead;  // some thread of this CTA gave up waiting (CTA-uniform after a barrier)
   const int n = a.n, tid = threadIdx.x;
-  if (tid == 0) s_dead = 0;
   float4* P = sm4;                   // positions {x, y, z, m} of the current state, j at j + j / chunk
   const int IB = a.I;                // i-particles per CTA (the last CTA may own fewer)
   float4* part = sm4 + n + a.nch;    // [nch][IB] chunk partials of this CTA's i
@@ -184,6 +182,7 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_leapfrog_small(const Small
     const uint4* src = a.pub + static_cast<size_t>(state & 1) * n;
     const unsigned int want = static_cast<unsigned int>(state);
     const unsigned long long t0 = globaltimer_ns();
+    bool dead = false;
 #pragma unroll
     for (int k0 = 0; k0 < kSmallGather; k0 += kSmallGather / 2) {  // two batches of in-flight loads
       constexpr int B = kSmallGather / 2;
@@ -211,13 +210,14 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_leapfrog_small(const Small
           }
         }
         if (todo && poll_expired(a.watch, t0, kFaultLeapfrogSmall)) {  // a CTA never published: give up
-          s_dead = 1;
+          dead = true;
           break;
         }
       }
     }
-    __syncthreads();
-    return s_dead == 0;  // false: leave without writing pos / vel / acc (b2_fault_status reports it)
+    // barrier + CTA-wide vote (no static shared memory: the dynamic allocation may use it all);
+    // false: leave without writing pos / vel / acc (b2_fault_status reports it)
+    return !__syncthreads_or(dead);
   };
 
   const float h = a.h;

@@ -51,7 +51,12 @@ void allow_max_dynamic_smem(const void* fn) {
   std::lock_guard<std::mutex> lk(mu);
   for (const auto& d : done)
     if (d.first == dev && d.second == fn) return;
-  cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, device_info().smem_optin);
+  // the opt-in limit covers static + dynamic shared memory
+  cudaFuncAttributes fa{};
+  const size_t stat = cudaFuncGetAttributes(&fa, fn) == cudaSuccess ? fa.sharedSizeBytes : 0;
+  const int dyn = device_info().smem_optin - static_cast<int>(stat);
+  if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn) != cudaSuccess)
+    cudaGetLastError();  // a later launch reports a real problem; never leave a sticky error here
   done.emplace_back(dev, fn);
 }
 
