@@ -201,19 +201,27 @@ def cpu_info() -> str:
 
 
 def nbody_sample_parity(pos_np, acc_np, n_sample: int = 512, what: str = "the e2e drop-in output"):
-    """Checker (oracle/_ref, the reference listing built -O3): a random i-sample of a full-size
-    force evaluation against all j. SURVEY §8d tolerance for N = 2^20: relL2 <= 1e-4."""
+    """Checker: a random i-sample of a full-size force evaluation against all j, compared with
+    the reference's own build (oracle/_ref libref_ieee, the listing at -O3) AND with the FP64
+    yardstick (oracle calc_acc_f64). The gate is the distance to FP64 (relL2 <= 1e-5, the fast
+    path's tolerance): at large N the reference's sequential FP32 j-sum is itself far from the
+    exact sum (3.5e-4 at N = 2^22, 2e-5 at 2^20), so "close to the reference" stops meaning
+    "correct" -- both distances are reported."""
     import numpy as np
 
     import oracle
 
     n = pos_np.shape[0]
-    idx = np.sort(np.random.default_rng(1234).choice(n, n_sample, replace=False))
-    want = oracle.Reference("ieee").calc_acc(np.ascontiguousarray(pos_np[idx]), pos_np, EPS)
-    got = acc_np[idx]
-    rel = float(np.linalg.norm(got[:, :3] - want[:, :3]) / np.linalg.norm(want[:, :3]))
-    return {"relL2_acc": rel, "tolerance": 1e-4, "ok": rel <= 1e-4,
-            "sample": f"{n_sample} random i x {n} j of {what} vs oracle/_ref libref_ieee"}
+    idx = np.sort(np.random.default_rng(1234).choice(n, min(n_sample, n), replace=False))
+    sample = np.ascontiguousarray(pos_np[idx])
+    want = oracle.Reference("ieee").calc_acc(sample, pos_np, EPS)[:, :3]
+    exact = oracle.Restatement().calc_acc_f64(sample, pos_np, EPS)[:, :3]
+    got = acc_np[idx][:, :3].astype(np.float64)
+    rel = lambda a, b: float(np.linalg.norm(a - b) / np.linalg.norm(b))  # noqa: E731
+    ours = rel(got, exact)
+    return {"relL2_acc": rel(got, want), "relL2_f64": ours, "ref_relL2_f64": rel(want, exact), "tolerance": 1e-5,
+            "ok": ours <= 1e-5,
+            "sample": f"{len(idx)} random i x {n} j of {what} vs libref_ieee and the FP64 yardstick"}
 
 
 def diffusion_parity(f0, got, steps, dargs):
@@ -1023,7 +1031,8 @@ def compact(full: dict) -> dict:
         out["e2e"] = {k: _r(e.get(k)) for k in ("value", "unit", "h2d_bytes_per_step", "d2h_bytes_per_step")}
     if full.get("parity"):
         pa = full["parity"]
-        out["parity"] = {k: _r(pa[k]) for k in ("relL2_acc", "tolerance", "ok", "shard_eq_unsharded") if k in pa}
+        out["parity"] = {k: _r(pa[k]) for k in ("relL2_f64", "ref_relL2_f64", "relL2_acc", "tolerance", "ok",
+                                                  "shard_eq_unsharded") if k in pa}
     sec = {}
     d = full.get("secondary", {}).get("diffusion")
     if d:

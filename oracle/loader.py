@@ -82,8 +82,19 @@ class Restatement(_Base):
                                                ctypes.c_int, ctypes.c_int, _f32p]
         L.oracle_kdk_update.argtypes = [ctypes.c_int, _f32p, _f32p, _f32p, _f32p, ctypes.c_int, ctypes.c_float,
                                         ctypes.c_float, ctypes.c_float, ctypes.c_int]
+        L.oracle_calc_acc_f64.argtypes = [ctypes.c_int, _f32p, ctypes.POINTER(ctypes.c_double), ctypes.c_int, _f32p,
+                                          ctypes.c_float]
         self._calc_acc = L.oracle_calc_acc
         self._diffusion3d = L.oracle_diffusion3d
+
+    def calc_acc_f64(self, ipos, jpos, eps) -> np.ndarray:
+        """FP64 yardstick (exact 1/sqrt, double sums): float64[Ni, 4], .w = the potential sum."""
+        ipos = np.ascontiguousarray(ipos, dtype=np.float32)
+        jpos = np.ascontiguousarray(jpos, dtype=np.float32)
+        out = np.zeros((ipos.shape[0], 4), np.float64)
+        self.lib.oracle_calc_acc_f64(ipos.shape[0], _ptr(ipos), out.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
+                                     jpos.shape[0], _ptr(jpos), ctypes.c_float(eps))
+        return out
 
     def calc_acc_partials(self, ipos, jpos, eps, chunk, potential=False, out=None):
         ipos = np.ascontiguousarray(ipos, dtype=np.float32)

@@ -137,3 +137,20 @@ def test_leapfrog_restatement_time_reversible(restatement):
     p2, v2, _ = restatement.leapfrog(p1, -v1, eps, dt, 8)
     assert rel_l2(p2[:, :3], pos[:, :3]) < 1e-5
     assert rel_l2(-v2[:, :3], vel[:, :3]) < 1e-4
+
+
+def test_f64_yardstick_and_reference_error_growth(restatement, reference):
+    """The FP64 yardstick (calc_acc_f64) agrees with the reference's IEEE build to the latter's
+    own FP32 error (~1e-6 at N=4096), and that error GROWS with N (sequential j-sum,
+    listing_nbody.c:8-24) -- why large-N parity is judged against FP64."""
+    from paper_2411_18889_b200.nbody import plummer_numpy
+
+    errs = []
+    for n in (4096, 65536):
+        pos, _ = plummer_numpy(n, 42)
+        sample = np.ascontiguousarray(pos[:: n // 64])
+        exact = restatement.calc_acc_f64(sample, pos, 2.0 ** -6)[:, :3]
+        ref = reference.calc_acc(sample, pos, 2.0 ** -6)[:, :3]
+        errs.append(float(np.linalg.norm(ref - exact) / np.linalg.norm(exact)))
+    assert errs[0] < 5e-6
+    assert errs[1] > errs[0]
