@@ -394,26 +394,24 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     sharded = world > 1 or args.dist
     n = args.n or ((1 << 20) if world == 1 else (1 << 22))
     pos_np, vel_np = b2.plummer_numpy(n, 42)
-    steady = _lib.B2_KDK_REDUCE | _lib.B2_KDK_KICK_END | _lib.B2_KDK_KICK_DRIFT
+    steady = _lib.B2_KDK_KICK_END | _lib.B2_KDK_KICK_DRIFT  # the force kernel reduces the partials itself
     hh = 0.5 * DT
     if not sharded:
         pos = torch.from_numpy(pos_np).to(dev)
         vel = torch.from_numpy(vel_np).to(dev)
-        nch = lib.b2_calc_acc_nchunks(n, 0)
-        part = torch.empty((nch * n, 4), dtype=torch.float32, device=dev)
+        ws = torch.empty(int(lib.b2_calc_acc_workspace_bytes(n, n, 0)), dtype=torch.uint8, device=dev)
         acc = torch.empty_like(pos)
         sh = _lib.stream_handle(dev)
 
-        def force():
-            _lib.check(lib.b2_calc_acc_partials(n, pos.data_ptr(), n, pos.data_ptr(), EPS, 0, part.data_ptr(), sh),
-                       "partials")
+        def force():  # k_force_fast with the in-kernel in-order reduction of the j-chunk partials
+            _lib.check(lib.b2_calc_acc(n, pos.data_ptr(), acc.data_ptr(), n, pos.data_ptr(), EPS, 0, ws.data_ptr(),
+                                       ws.numel(), sh), "calc_acc")
 
         def update(phases):
-            _lib.check(lib.b2_kdk_update(n, pos.data_ptr(), vel.data_ptr(), acc.data_ptr(), part.data_ptr(), nch,
+            _lib.check(lib.b2_kdk_update(n, pos.data_ptr(), vel.data_ptr(), acc.data_ptr(), None, 1,
                                          hh, hh, DT, phases, sh), "update")
 
         force()
-        update(_lib.B2_KDK_REDUCE)
         update(_lib.B2_KDK_KICK_DRIFT)
 
         def step(evs):
@@ -440,12 +438,12 @@ def run_ours(args, rank: int, world: int, local_rank: int):
             else:
                 sim._await_peers()
             evs[3].record(stream)
-            sim.k.partials(sim.pos, sim.pos_all, sim.eps, sim.part)
+            sim._force()
             evs[1].record(stream)
             if sim.transport == "nccl":
-                sim.k.update(sim.pos, sim.vel, sim.acc, sim.part, sim.nch, hh, hh, DT, steady)
+                sim.k.update(sim.pos, sim.vel, sim.acc, sim.part, sim.nch, hh, hh, DT, steady | sim.reduce_phase)
             else:
-                sim._publish_update(sim.vel, sim.part, hh, hh, DT, steady)
+                sim._publish_update(sim.vel, sim.part, hh, hh, DT, steady | sim.reduce_phase)
             evs[2].record(stream)
 
         parallelism = f"i-shard x{world}, " + ("NCCL all_gather_into_tensor of positions" if sim.transport == "nccl"
@@ -606,9 +604,8 @@ def nbody_sharded_parity(ctx, sim, n):
         acc_full = torch.empty_like(allpos)
         b2.calc_acc(n, allpos, acc_full, n, allpos, EPS)
         # the sharded force of rank 0's shard at the same positions
-        sim.k.partials(sim.pos, sim.pos_all, sim.eps, sim.part)
         mine = torch.empty_like(sim.pos)
-        sim.k.update(None, None, mine, sim.part, sim.nch, 0.0, 0.0, 0.0, 1)
+        sim.k.force(sim.pos, sim.pos_all, sim.eps, mine, sim.ws)
         same = bool(torch.equal(mine.view(torch.int32), acc_full[:sim.pos.shape[0]].view(torch.int32)))
         try:
             out = nbody_sample_parity(allpos.cpu().numpy(), acc_full.cpu().numpy(),
@@ -634,13 +631,13 @@ def nbody_p2p_leg(ctx, pos_np, vel_np, n):
                           torch.from_numpy(vel_np[lo:lo + nl]).to(ctx.dev), EPS, DT, transport="p2p")
     try:
         sim.step(1, close=False)
-        hh, steady = 0.5 * DT, _lib.B2_KDK_REDUCE | _lib.B2_KDK_KICK_END | _lib.B2_KDK_KICK_DRIFT
+        hh, steady = 0.5 * DT, _lib.B2_KDK_KICK_END | _lib.B2_KDK_KICK_DRIFT
 
         def step(evs):
             evs[0].record(ctx.stream)
             sim._await_peers()
-            sim.k.partials(sim.pos, sim.pos_all, sim.eps, sim.part)
-            sim._publish_update(sim.vel, sim.part, hh, hh, DT, steady)
+            sim._force()
+            sim._publish_update(sim.vel, sim.part, hh, hh, DT, steady | sim.reduce_phase)
             evs[1].record(ctx.stream)
 
         steps = max(1, min(ctx.args.steps, 3))

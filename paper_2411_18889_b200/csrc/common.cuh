@@ -38,7 +38,8 @@ struct Watch {
 };
 Watch make_watch();
 // fault codes (which kernel gave up), reported by b2_fault_status / b2_fault_kernel
-constexpr unsigned int kFaultLeapfrogSmall = 1, kFaultResident = 2, kFaultSlabEdges = 3, kFaultHalo2 = 4;
+constexpr unsigned int kFaultLeapfrogSmall = 1, kFaultResident = 2, kFaultSlabEdges = 3, kFaultHalo2 = 4,
+                       kFaultForceRing = 5;
 
 // ---- Device helpers shared by the persistent kernels (k_leapfrog_small,
 // k_diffusion_resident): 16-byte words a producer CTA publishes and a consumer
@@ -92,6 +93,13 @@ __device__ __forceinline__ unsigned long long globaltimer_ns() {
 // leaves its loops and exits normally: no __trap, the context stays usable.
 __device__ __forceinline__ bool poll_expired(const Watch& w, unsigned long long t0, unsigned int code) {
   if (w.fault && *reinterpret_cast<volatile unsigned int*>(w.fault)) return true;
+  if (globaltimer_ns() - t0 <= w.timeout_ns) return false;
+  if (w.fault) atomicCAS(w.fault, 0u, code);
+  return true;
+}
+// The same without the early exit on a standing fault: for waits whose giving up would
+// corrupt data rather than merely skip work (a ring slot still being read).
+__device__ __forceinline__ bool poll_timed_out(const Watch& w, unsigned long long t0, unsigned int code) {
   if (globaltimer_ns() - t0 <= w.timeout_ns) return false;
   if (w.fault) atomicCAS(w.fault, 0u, code);
   return true;

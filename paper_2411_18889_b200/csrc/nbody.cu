@@ -93,6 +93,40 @@ __device__ __forceinline__ void interact_mixed(const float2 X, const float2 Y, c
   }
 }
 
+// In-kernel, in-order reduction of the j-chunk partials (FUSED = true).
+// Work items (i-tile, chunk) are handed out in order by a ticket counter, chunk-minor, so
+// the nch CTAs of one i-tile run at about the same time. Each writes its partial tile
+// into ring slot itile % R of an L2-sized ring (R tiles of nch x BLOCK*IPT float4) and
+// arrives on the slot's counter; the LAST arriving CTA sums the slot's partials in the
+// fixed order c = 0, 1, ..., nch-1 -- the order k_kdk_update uses, so the bits are
+// those of the two-kernel path -- writes acc, drops the slot's lines from L2 without
+// write-back (discard.global.L2) and opens the slot for i-tile itile + R. A CTA waits
+// for its slot only if the reduction of i-tile itile - R is still running: every CTA it
+// could wait for took an earlier ticket and is resident, so the wait always ends (and
+// the watchdog bounds it anyway). Scratch: R * nch * tile * 16 B (8 MiB at N = 2^20)
+// instead of nch * Ni * 16 B (1 GiB), and the partials never reach HBM.
+struct Fused {
+  float4* ring;         // [R][nch][tile] partial tiles
+  unsigned int* ctrl;   // [0] ticket, [1..R] arrivals per slot, [1+R .. 1+2R) tiles through each slot
+  float4* acc;          // [Ni] result
+  int R;                // ring slots
+  Watch watch;
+};
+constexpr int kRingSlots = 8;
+constexpr size_t kRingCtrlBytes = 256;  // ctrl words (zeroed by the host before each launch)
+
+__device__ __forceinline__ unsigned int ld_acquire_u32(const unsigned int* p) {
+  unsigned int v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_u32(unsigned int* p, unsigned int v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void discard_l2_line(const void* p) {
+  asm volatile("discard.global.L2 [%0], 128;" ::"l"(p) : "memory");
+}
+
 // SCHED: 0 depth-first / 1 breadth-first source order (ptxas mostly reschedules).
 // SCHED 2: j-values kept NON-duplicated in shared memory and fed to the packed
 // ops as scalar-broadcast operands (FADD2 R, R.F32x2, R.F32): one LDS.128 per j
@@ -104,19 +138,29 @@ __device__ __forceinline__ void interact_mixed(const float2 X, const float2 Y, c
 // trades FMA-pipe work for MUFU work: m r^-3 = ex2(fma(-1.5, lg2(r2), lg2(m)))
 // -- 2 MUFU + 1 FFMA2 per pair instead of 1 MUFU + 3 FMUL2 -- so the FP32
 // pipe (the binding one) and the MUFU pipe (58% busy) are balanced.
-template <int BLOCK, int kIPT, int MINB, int UNR, int SCHED, int ALT, bool POT>
+template <int BLOCK, int kIPT, int MINB, int UNR, int SCHED, int ALT, bool POT, bool FUSED>
 __global__ void __launch_bounds__(BLOCK, MINB)
     k_force_fast(const float4* __restrict__ ipos, int Ni, const float4* __restrict__ jpos, int Nj,
-                 int jchunk, int n_itiles, float eps2, float4* __restrict__ out) {
+                 int jchunk, int n_itiles, float eps2, float4* __restrict__ out, const Fused fz) {
   constexpr int P = kIPT / 2;
   constexpr int DUP = SCHED >= 2 ? 1 : 2;  // float4 slots per j in shared memory
   static_assert(ALT == 0 || DUP == 1, "ALT path uses scalar-broadcast j");
   __shared__ float4 sj[2][DUP * BLOCK];
   __shared__ float slm[2][ALT > 0 ? BLOCK : 1];
+  __shared__ int s_item, s_last;
 
   const int tid = threadIdx.x;
-  const int itile = blockIdx.x % n_itiles;
-  const int chunk = blockIdx.x / n_itiles;
+  const int nch = gridDim.x / n_itiles;
+  int itile, chunk;
+  if (FUSED) {  // in-order work items, chunk-minor: the chunks of an i-tile run together
+    if (tid == 0) s_item = static_cast<int>(atomicAdd(fz.ctrl, 1u));
+    __syncthreads();
+    itile = s_item / nch;
+    chunk = s_item - itile * nch;
+  } else {
+    itile = blockIdx.x % n_itiles;
+    chunk = blockIdx.x / n_itiles;
+  }
   const int ibase = itile * (BLOCK * kIPT) + tid;
 
   float2 nx[P], ny[P], nz[P];
@@ -195,13 +239,78 @@ __global__ void __launch_bounds__(BLOCK, MINB)
     __syncthreads();
   }
 
-  float4* __restrict__ o = out + static_cast<size_t>(chunk) * Ni;
+  if (!FUSED) {
+    float4* __restrict__ o = out + static_cast<size_t>(chunk) * Ni;
 #pragma unroll
-  for (int p = 0; p < P; ++p) {
-    const int ia = ibase + (2 * p) * BLOCK;
-    const int ib = ibase + (2 * p + 1) * BLOCK;
-    if (ia < Ni) o[ia] = make_float4(ax[p].x, ay[p].x, az[p].x, POT ? ap[p].x : 0.f);
-    if (ib < Ni) o[ib] = make_float4(ax[p].y, ay[p].y, az[p].y, POT ? ap[p].y : 0.f);
+    for (int p = 0; p < P; ++p) {
+      const int ia = ibase + (2 * p) * BLOCK;
+      const int ib = ibase + (2 * p + 1) * BLOCK;
+      if (ia < Ni) o[ia] = make_float4(ax[p].x, ay[p].x, az[p].x, POT ? ap[p].x : 0.f);
+      if (ib < Ni) o[ib] = make_float4(ax[p].y, ay[p].y, az[p].y, POT ? ap[p].y : 0.f);
+    }
+    return;
+  }
+  // ---- fused: partial tile -> ring slot; the last chunk of the i-tile reduces in order ----
+  constexpr int TILE = BLOCK * kIPT;
+  const int R = fz.R, slot = itile % R;
+  unsigned int* arrive = fz.ctrl + 1 + slot;
+  unsigned int* gate = fz.ctrl + 1 + R + slot;  // i-tiles that went through this slot
+  if (tid == 0) {  // slot free? (i-tile itile - R reduced); almost never waits
+    const unsigned int want = static_cast<unsigned int>(itile / R);
+    const unsigned long long t0 = globaltimer_ns();
+    while (ld_acquire_u32(gate) != want)
+      if (poll_timed_out(fz.watch, t0, kFaultForceRing)) break;
+  }
+  __syncthreads();
+  float4* __restrict__ tile = fz.ring + static_cast<size_t>(slot) * nch * TILE;
+  {
+    float4* __restrict__ o = tile + static_cast<size_t>(chunk) * TILE;
+#pragma unroll
+    for (int p = 0; p < P; ++p) {
+      o[tid + (2 * p) * BLOCK] = make_float4(ax[p].x, ay[p].x, az[p].x, POT ? ap[p].x : 0.f);
+      o[tid + (2 * p + 1) * BLOCK] = make_float4(ax[p].y, ay[p].y, az[p].y, POT ? ap[p].y : 0.f);
+    }
+  }
+  __syncthreads();
+  if (tid == 0) {
+    __threadfence();  // publish this CTA's partials before arriving
+    s_last = atomicAdd(arrive, 1u) == static_cast<unsigned int>(nch - 1);
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();  // acquire side: the other chunks' partials are visible
+  // fixed summation order c = 0, 1, ..., nch-1 (as k_kdk_update): batches of loads in flight
+#pragma unroll 1
+  for (int e = 0; e < kIPT; ++e) {
+    const int il = tid + e * BLOCK;
+    const float4* __restrict__ col = tile + il;
+    float4 a = __ldcg(col);
+    constexpr int B = 16;
+    for (int c0 = 1; c0 < nch; c0 += B) {
+      float4 q[B];
+#pragma unroll
+      for (int b = 0; b < B; ++b)
+        if (c0 + b < nch) q[b] = __ldcg(col + static_cast<size_t>(c0 + b) * TILE);
+#pragma unroll
+      for (int b = 0; b < B; ++b) {
+        if (c0 + b < nch) {
+          a.x = __fadd_rn(a.x, q[b].x);
+          a.y = __fadd_rn(a.y, q[b].y);
+          a.z = __fadd_rn(a.z, q[b].z);
+          a.w = __fadd_rn(a.w, q[b].w);
+        }
+      }
+    }
+    const int i = itile * TILE + il;
+    if (i < Ni) fz.acc[i] = a;
+  }
+  __syncthreads();  // every read of the slot is done
+  // drop the slot's lines from L2 without writing them back: the partials never reach HBM
+  for (size_t l = tid; l < static_cast<size_t>(nch) * TILE / 8; l += BLOCK) discard_l2_line(tile + 8 * l);
+  __syncthreads();
+  if (tid == 0) {
+    *arrive = 0u;
+    st_release_u32(gate, static_cast<unsigned int>(itile / R + 1));  // open the slot for itile + R
   }
 }
 
@@ -320,15 +429,29 @@ __global__ void __launch_bounds__(128)
 
 
 // Launch variants of the fast kernel: {threads, i per thread, min CTAs/SM, j unroll}.
+using ForceFn = void (*)(const float4*, int, const float4*, int, int, int, float, float4*, const Fused);
 struct ForceVariant {
   int block, ipt;
-  void (*fn[2])(const float4*, int, const float4*, int, int, int, float, float4*);
+  ForceFn fn[2];     // partials out [nch][Ni] (potential off / on)
+  ForceFn fused[2];  // in-kernel reduction (nullptr: not instantiated for this variant)
 };
-#define B2_FV(B, I, M, U, S, A) \
-  { B, I, { k_force_fast<B, I, M, U, S, A, false>, k_force_fast<B, I, M, U, S, A, true> } }
+#define B2_FV(B, I, M, U, S, A)                                                                    \
+  {                                                                                                \
+    B, I, {k_force_fast<B, I, M, U, S, A, false, false>, k_force_fast<B, I, M, U, S, A, true, false>}, \
+    {                                                                                              \
+      nullptr, nullptr                                                                             \
+    }                                                                                              \
+  }
+#define B2_FVF(B, I, M, U, S, A)                                                                   \
+  {                                                                                                \
+    B, I, {k_force_fast<B, I, M, U, S, A, false, false>, k_force_fast<B, I, M, U, S, A, true, false>}, \
+    {                                                                                              \
+      k_force_fast<B, I, M, U, S, A, false, true>, k_force_fast<B, I, M, U, S, A, true, true>      \
+    }                                                                                              \
+  }
 static const ForceVariant kVariants[] = {
-    B2_FV(128, 16, 2, 1, 2, 0),  // 0: default for large N (best of the round-1 sweep)
-    B2_FV(64, 8, 8, 4, 1, 0),    // 1: medium N (more CTAs)
+    B2_FVF(128, 16, 2, 1, 2, 0),  // 0: default for large N (best of the round-1 sweep)
+    B2_FVF(64, 8, 8, 4, 1, 0),    // 1: medium N (more CTAs)
     B2_FV(256, 8, 2, 4, 0, 0),   // 2: round-1 first version
     B2_FV(256, 12, 1, 2, 1, 0),  // 3: duplicated-pair j
     B2_FV(128, 16, 2, 1, 3, 2),  // 4: 2 of 8 pairs on ex2/lg2
@@ -337,9 +460,10 @@ static const ForceVariant kVariants[] = {
     B2_FV(256, 12, 1, 2, 3, 1),  // 7: 1 of 6
     B2_FV(128, 16, 2, 2, 3, 2),  // 8
     B2_FV(256, 8, 2, 4, 3, 1),   // 9: 1 of 4
-    B2_FV(64, 2, 16, 4, 2, 0),   // 10: small N (configs[0]: N=4096)
+    B2_FVF(64, 2, 16, 4, 2, 0),  // 10: small N (configs[0]: N=4096)
 };
 #undef B2_FV
+#undef B2_FVF
 
 static int env_int_nb(const char* name, int dflt) {
   const char* e = std::getenv(name);
@@ -353,6 +477,48 @@ static int large_variant() {
     return (x >= 0 && x < static_cast<int>(sizeof(kVariants) / sizeof(kVariants[0]))) ? x : 0;
   }();
   return v;
+}
+
+// The variant launch_partials / launch_fused take for Ni (same per-lane arithmetic and j
+// order in every variant, so the choice never moves a bit).
+static const ForceVariant* pick_variant(int Ni, int nch, bool need_fused) {
+  const ForceVariant* v = &kVariants[large_variant()];
+  if (need_fused && !v->fused[0]) v = &kVariants[0];
+  static const long long want_k = std::max(0, env_int_nb("SOLOMON_NBODY_WANT", 4));  // tuning knob: CTAs per SM
+  const long long want = want_k * device_info().sms;
+  auto ctas = [&](const ForceVariant* c) { return (long long)((Ni + c->block * c->ipt - 1) / (c->block * c->ipt)) * nch; };
+  // below that, 64 x 8 only while it still gives >= 16 CTAs per SM; else 64 x 2 (N = 8192:
+  // 1598 vs 1455 Ginteractions/s, scripts/midn_sweep.py).
+  if (ctas(v) < want) v = ctas(&kVariants[1]) >= 4 * want ? &kVariants[1] : &kVariants[10];
+  return v;
+}
+
+constexpr int kMaxTile = 2048;  // largest BLOCK * IPT of a fused variant
+
+static size_t fused_workspace_bytes(int Ni, int Nj, int flags) {
+  const int nch = nchunks_for(Nj, flags);
+  const size_t rows = std::min<size_t>(static_cast<size_t>(kRingSlots) * kMaxTile,
+                                       static_cast<size_t>(std::max(Ni, 0)) + kMaxTile);
+  return kRingCtrlBytes + 128 + static_cast<size_t>(nch) * rows * sizeof(float4);
+}
+
+// Force with the in-kernel in-order reduction: acc = sum_c partials_c (bits of partials +
+// B2_KDK_REDUCE). ws >= fused_workspace_bytes; one memset of the control words + one launch.
+static int launch_fused(int Ni, const float4* ipos, int Nj, const float4* jpos, float eps, int flags, float4* acc,
+                        void* ws, cudaStream_t s) {
+  const int jchunk = chunk_size(Nj, flags);
+  const int nch = nchunks_for(Nj, flags);
+  const ForceVariant* v = pick_variant(Ni, nch, true);
+  const int tile = v->block * v->ipt;
+  const int nit = (Ni + tile - 1) / tile;
+  unsigned int* ctrl = static_cast<unsigned int*>(ws);
+  const uintptr_t rb = (reinterpret_cast<uintptr_t>(ws) + kRingCtrlBytes + 127) & ~static_cast<uintptr_t>(127);
+  Fused fz{reinterpret_cast<float4*>(rb), ctrl, acc, std::min(kRingSlots, nit), make_watch()};
+  cudaError_t e = cudaMemsetAsync(ctrl, 0, kRingCtrlBytes, s);
+  if (e != cudaSuccess) return static_cast<int>(e);
+  v->fused[(flags & B2_POTENTIAL) ? 1 : 0]<<<nit * nch, v->block, 0, s>>>(ipos, Ni, jpos, Nj, jchunk, nit, eps * eps,
+                                                                       acc, fz);
+  return launch_status();
 }
 
 static int launch_partials(int Ni, const float4* ipos, int Nj, const float4* jpos, float eps, int flags,
@@ -369,19 +535,11 @@ static int launch_partials(int Ni, const float4* ipos, int Nj, const float4* jpo
   }
   const int jchunk = chunk_size(Nj, flags);
   const int nch = nchunks_for(Nj, flags);
-  // Largest tile whose (i-tile, j-chunk) grid still fills the 148 SMs: the
-  // tuned large variant, else 64x8, else 64x2 (small N is latency-bound and
-  // needs every warp it can get).
-  const ForceVariant* v = &kVariants[large_variant()];
-  static const long long want_k = std::max(0, env_int_nb("SOLOMON_NBODY_WANT", 4));  // tuning knob: CTAs per SM
-  const long long want = want_k * device_info().sms;
-  auto ctas = [&](const ForceVariant* c) { return (long long)((Ni + c->block * c->ipt - 1) / (c->block * c->ipt)) * nch; };
-  // below that, 64 x 8 only while it still gives >= 16 CTAs per SM; else 64 x 2 (N = 8192:
-  // 1598 vs 1455 Ginteractions/s, scripts/midn_sweep.py). Same per-lane arithmetic and j
-  // order in every variant, so the choice does not move a bit.
-  if (ctas(v) < want) v = ctas(&kVariants[1]) >= 4 * want ? &kVariants[1] : &kVariants[10];
+  // Largest tile whose (i-tile, j-chunk) grid still fills the 148 SMs: the tuned large
+  // variant, else 64x8, else 64x2 (small N is latency-bound and needs every warp it can get).
+  const ForceVariant* v = pick_variant(Ni, nch, false);
   const int nit = (Ni + v->block * v->ipt - 1) / (v->block * v->ipt);
-  v->fn[pot ? 1 : 0]<<<nit * nch, v->block, 0, s>>>(ipos, Ni, jpos, Nj, jchunk, nit, eps2, out);
+  v->fn[pot ? 1 : 0]<<<nit * nch, v->block, 0, s>>>(ipos, Ni, jpos, Nj, jchunk, nit, eps2, out, Fused{});
   return launch_status();
 }
 
@@ -416,7 +574,7 @@ int b2_calc_acc_nchunks(int Nj, int flags) { return nchunks_for(Nj, flags); }
 size_t b2_calc_acc_workspace_bytes(int Ni, int Nj, int flags) {
   const int nch = nchunks_for(Nj, flags);
   if (nch <= 1 || Ni <= 0) return 0;
-  return static_cast<size_t>(nch) * static_cast<size_t>(Ni) * sizeof(float4);
+  return fused_workspace_bytes(Ni, Nj, flags);
 }
 
 int b2_calc_acc_partials(int Ni, const float* ipos, int Nj, const float* jpos, float eps, int flags,
@@ -452,12 +610,8 @@ int b2_calc_acc(int Ni, const float* ipos, float* iacc, int Nj, const float* jpo
                            flags, reinterpret_cast<float4*>(iacc), s);
   if (workspace_bytes < b2_calc_acc_workspace_bytes(Ni, Nj, flags)) return B2_ESPACE;
   if (!aligned16(workspace)) return B2_EALIGN;
-  float4* part = static_cast<float4*>(workspace);
-  if ((rc = launch_partials(Ni, reinterpret_cast<const float4*>(ipos), Nj, reinterpret_cast<const float4*>(jpos), eps,
-                            flags, part, s)))
-    return rc;
-  return launch_update(Ni, nullptr, nullptr, reinterpret_cast<float4*>(iacc), part, nch, 0.f, 0.f, 0.f,
-                       B2_KDK_REDUCE, s);
+  return launch_fused(Ni, reinterpret_cast<const float4*>(ipos), Nj, reinterpret_cast<const float4*>(jpos), eps,
+                      flags, reinterpret_cast<float4*>(iacc), workspace, s);
 }
 
 int b2_kdk_update(int n, float* pos, float* vel, float* acc, const float* partials, int nchunks, float h_end,
@@ -498,8 +652,9 @@ int b2_kdk_update_publish(int n, const float* pos_in, float* pos_out, float* vel
 }
 
 size_t b2_leapfrog_workspace_bytes(int n, int flags) {
-  const int nch = nchunks_for(n, flags & (B2_POTENTIAL | B2_EXACT));
-  return static_cast<size_t>(std::max(nch, 1)) * static_cast<size_t>(std::max(n, 0)) * sizeof(float4);
+  const int ff = flags & (B2_POTENTIAL | B2_EXACT);
+  // the fused force's ring, or the persistent small-N path's [2][n] position words
+  return std::max(b2_calc_acc_workspace_bytes(n, n, ff), 2 * static_cast<size_t>(std::max(n, 0)) * sizeof(uint4));
 }
 
 int b2_leapfrog(int n, float* pos, float* vel, float* acc, float eps, float dt, int nsteps, int flags,
@@ -516,21 +671,20 @@ int b2_leapfrog(int n, float* pos, float* vel, float* acc, float eps, float dt, 
   float4* V = reinterpret_cast<float4*>(vel);
   float4* A = reinterpret_cast<float4*>(acc);
   if (launch_leapfrog_small(n, P, V, A, eps, dt, nsteps, flags, workspace, workspace_bytes, s)) return B2_OK;
-  float4* part = static_cast<float4*>(workspace);
-  const int nch = nchunks_for(n, fflags);
   const float h = 0.5f * dt;
-  if (flags & B2_INIT_ACC) {
-    if ((rc = launch_partials(n, P, n, P, eps, fflags, part, s))) return rc;
-    if ((rc = launch_update(n, P, V, A, part, nch, 0.f, 0.f, 0.f, B2_KDK_REDUCE, s))) return rc;
-  }
+  // a = calc_acc(x) with the chunk partials reduced in order inside the force kernel
+  auto force = [&]() {
+    return b2_calc_acc(n, pos, acc, n, pos, eps, fflags, workspace, workspace_bytes, s);
+  };
+  if ((flags & B2_INIT_ACC) && (rc = force())) return rc;
   if (nsteps == 0) return B2_OK;
   // step 0 opening kick + drift
-  if ((rc = launch_update(n, P, V, A, nullptr, nch, 0.f, h, dt, B2_KDK_KICK_DRIFT, s))) return rc;
+  if ((rc = launch_update(n, P, V, A, nullptr, 1, 0.f, h, dt, B2_KDK_KICK_DRIFT, s))) return rc;
   for (int st = 0; st < nsteps; ++st) {
-    if ((rc = launch_partials(n, P, n, P, eps, fflags, part, s))) return rc;
+    if ((rc = force())) return rc;
     const bool last = st + 1 == nsteps;
-    const int ph = B2_KDK_REDUCE | B2_KDK_KICK_END | (last ? 0 : B2_KDK_KICK_DRIFT);
-    if ((rc = launch_update(n, P, V, A, part, nch, h, h, dt, ph, s))) return rc;
+    const int ph = B2_KDK_KICK_END | (last ? 0 : B2_KDK_KICK_DRIFT);
+    if ((rc = launch_update(n, P, V, A, nullptr, 1, h, h, dt, ph, s))) return rc;
   }
   return B2_OK;
 }

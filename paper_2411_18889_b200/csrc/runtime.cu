@@ -139,6 +139,7 @@ const char* b2_fault_kernel(int which) {
     case kFaultResident: return "k_diffusion_resident (face words of another brick)";
     case kFaultSlabEdges: return "k_diffusion_slab_edges (a neighbour rank's halo rows)";
     case kFaultHalo2: return "k_diffusion_slab_halo2 (a neighbour rank's two halo planes)";
+    case kFaultForceRing: return "k_force_fast (a ring slot of the in-kernel chunk reduction)";
     default: return "unknown kernel";
   }
 }

@@ -48,6 +48,16 @@ class CudaNBodyKernels:
     def nchunks(self, nj: int) -> int:
         return self.lib.b2_calc_acc_nchunks(nj, self.flags)
 
+    def workspace_bytes(self, ni: int, nj: int) -> int:
+        return int(self.lib.b2_calc_acc_workspace_bytes(ni, nj, self.flags))
+
+    def force(self, ipos: torch.Tensor, jpos: torch.Tensor, eps: float, acc: torch.Tensor, ws: torch.Tensor) -> None:
+        """acc = calc_acc(ipos, jpos) with the chunk partials reduced in order inside the kernel
+        (b2_calc_acc; the same bits as partials + B2_KDK_REDUCE)."""
+        _lib.check(self.lib.b2_calc_acc(ipos.shape[0], ipos.data_ptr(), acc.data_ptr(), jpos.shape[0],
+                                        jpos.data_ptr(), float(eps), self.flags, ws.data_ptr(), ws.numel(),
+                                        _lib.stream_handle(ipos.device)), "calc_acc")
+
     def partials(self, ipos: torch.Tensor, jpos: torch.Tensor, eps: float, out: torch.Tensor) -> None:
         _lib.check(self.lib.b2_calc_acc_partials(ipos.shape[0], ipos.data_ptr(), jpos.shape[0], jpos.data_ptr(),
                                                  float(eps), self.flags, out.data_ptr(),
@@ -189,14 +199,35 @@ class ShardedLeapfrog:
         self.acc = torch.empty_like(self.pos)
         self.eps, self.dt = float(eps), float(dt)
         self.nch = self.k.nchunks(self.plan.n_total)
-        self.part = torch.empty((max(self.nch, 1) * n_local, 4), dtype=torch.float32, device=dev)
+        # CUDA kernels: the force kernel reduces the chunk partials itself (L2 ring workspace);
+        # injected test kernels: partials [nch][n_local] + the update's in-order reduce
+        self.fused = hasattr(self.k, "force")
+        if self.fused:
+            self.ws = torch.empty(max(self.k.workspace_bytes(n_local, self.plan.n_total), 16), dtype=torch.uint8,
+                                  device=dev)
+            self.part = None
+        else:
+            self.part = torch.empty((max(self.nch, 1) * n_local, 4), dtype=torch.float32, device=dev)
         self._opened = False
         self.steps = 0
         if transport == "p2p":
             self._setup_p2p()
         self.gather()
-        self.k.partials(self.pos, self.pos_all, self.eps, self.part)
-        self.k.update(None, None, self.acc, self.part, self.nch, 0.0, 0.0, 0.0, B2_KDK_REDUCE)
+        self._force()
+        if not self.fused:
+            self.k.update(None, None, self.acc, self.part, self.nch, 0.0, 0.0, 0.0, B2_KDK_REDUCE)
+
+    def _force(self) -> None:
+        """This shard's accelerations from pos_all (fused: into acc; else: partials)."""
+        if self.fused:
+            self.k.force(self.pos, self.pos_all, self.eps, self.acc, self.ws)
+        else:
+            self.k.partials(self.pos, self.pos_all, self.eps, self.part)
+
+    @property
+    def reduce_phase(self) -> int:
+        """B2_KDK_REDUCE when the update must reduce partials (unfused kernels), else 0."""
+        return 0 if self.fused else B2_KDK_REDUCE
 
     @property
     def pos_all(self) -> torch.Tensor:
@@ -311,9 +342,9 @@ class ShardedLeapfrog:
                     self.k.update(self.pos, self.vel, self.acc, None, self.nch, 0.0, h, self.dt, B2_KDK_KICK_DRIFT)
                     self._opened = True
                 self.gather()
-                self.k.partials(self.pos, self.pos_all, self.eps, self.part)
+                self._force()
                 last = close and s + 1 == nsteps
-                phases = B2_KDK_REDUCE | B2_KDK_KICK_END | (0 if last else B2_KDK_KICK_DRIFT)
+                phases = self.reduce_phase | B2_KDK_KICK_END | (0 if last else B2_KDK_KICK_DRIFT)
                 self.k.update(self.pos, self.vel, self.acc, self.part, self.nch, h, h, self.dt, phases)
                 self._opened = not last
             else:
@@ -324,9 +355,9 @@ class ShardedLeapfrog:
                     self._publish_update(self.vel, None, 0.0, h, self.dt, B2_KDK_KICK_DRIFT)
                     self._opened = True
                 self._await_peers()
-                self.k.partials(self.pos, self.pos_all, self.eps, self.part)
+                self._force()
                 last = close and s + 1 == nsteps
-                phases = B2_KDK_REDUCE | B2_KDK_KICK_END | (0 if last else B2_KDK_KICK_DRIFT)
+                phases = self.reduce_phase | B2_KDK_KICK_END | (0 if last else B2_KDK_KICK_DRIFT)
                 self._publish_update(self.vel, self.part, h, h, self.dt, phases)
                 self._opened = not last
             self.steps += 1

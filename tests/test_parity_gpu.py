@@ -124,6 +124,36 @@ def test_chunking_depends_on_nj_only(b2):
             assert torch.equal(part, full[r * sl:(r + 1) * sl])
 
 
+@pytest.mark.parametrize("ni,nj,pot", [(1 << 17, 4096, False), (70001, 9000, True), (2048, 1 << 16, False),
+                                       (300, 5000, True), (1 << 20, 1 << 12, False)])
+def test_fused_force_reduction_bit_identical_to_partials(b2, ni, nj, pot):
+    """k_force_fast's in-kernel reduction (ticketed work items, L2 ring of partial tiles, the
+    last chunk of an i-tile sums c = 0..nch-1) == b2_calc_acc_partials + the update kernel's
+    in-order B2_KDK_REDUCE, bit for bit -- with many i-tiles per ring slot (ring reuse),
+    ragged last tiles and the potential."""
+    from paper_2411_18889_b200 import _lib
+
+    lib = _lib.load()
+    rng = np.random.default_rng(ni + nj)
+    ipos = dev(rng.normal(size=(ni, 4)).astype(np.float32) * np.float32([1, 1, 1, 0]) + np.float32([0, 0, 0, 1e-3]))
+    jpos = dev(rng.normal(size=(nj, 4)).astype(np.float32) * np.float32([1, 1, 1, 0]) + np.float32([0, 0, 0, 1e-3]))
+    flags = _lib.B2_POTENTIAL if pot else 0
+    nch = lib.b2_calc_acc_nchunks(nj, flags)
+    part = torch.empty((nch * ni, 4), device="cuda")
+    want = torch.empty((ni, 4), device="cuda")
+    sh = _lib.stream_handle()
+    assert lib.b2_calc_acc_partials(ni, ipos.data_ptr(), nj, jpos.data_ptr(), 0.01, flags, part.data_ptr(), sh) == 0
+    assert lib.b2_kdk_update(ni, None, None, want.data_ptr(), part.data_ptr(), nch, 0.0, 0.0, 0.0, 1, sh) == 0
+    ws = torch.empty(int(lib.b2_calc_acc_workspace_bytes(ni, nj, flags)), dtype=torch.uint8, device="cuda")
+    assert ws.numel() < part.numel() * 4 or nch * ni <= 8 * 2048 * nch  # the ring, not nch x Ni x 16 B
+    got = torch.full((ni, 4), float("nan"), device="cuda")
+    for _ in range(3):  # repeated launches reuse the ring and its control words
+        assert lib.b2_calc_acc(ni, ipos.data_ptr(), got.data_ptr(), nj, jpos.data_ptr(), 0.01, flags, ws.data_ptr(),
+                               ws.numel(), sh) == 0
+    _lib.check_fault()
+    assert torch.equal(got.view(torch.int32), want.view(torch.int32))
+
+
 @pytest.mark.parametrize("exact", [True, False])
 def test_leapfrog_config0_16_steps(b2, restatement, exact):
     """BASELINE config[0]: N=4096 Plummer, 16 KDK steps, vs the CPU KDK around the oracle calc_acc."""
