@@ -93,27 +93,31 @@ __device__ __forceinline__ void interact_mixed(const float2 X, const float2 Y, c
   }
 }
 
-// In-kernel, in-order reduction of the j-chunk partials (FUSED = true).
-// Work items (i-tile, chunk) are handed out in order by a ticket counter, chunk-minor, so
-// the nch CTAs of one i-tile run at about the same time. Each writes its partial tile
-// into ring slot itile % R of an L2-sized ring (R tiles of nch x BLOCK*IPT float4) and
-// arrives on the slot's counter; the LAST arriving CTA sums the slot's partials in the
-// fixed order c = 0, 1, ..., nch-1 -- the order k_kdk_update uses, so the bits are
-// those of the two-kernel path -- writes acc, drops the slot's lines from L2 without
-// write-back (discard.global.L2) and opens the slot for i-tile itile + R. A CTA waits
-// for its slot only if the reduction of i-tile itile - R is still running: every CTA it
-// could wait for took an earlier ticket and is resident, so the wait always ends (and
-// the watchdog bounds it anyway). Scratch: R * nch * tile * 16 B (8 MiB at N = 2^20)
-// instead of nch * Ni * 16 B (1 GiB), and the partials never reach HBM.
+// In-kernel, in-order reduction of the j-chunk partials (Fused.ring set).
+// The grid is ordered chunk-minor (blockIdx = itile * nch + chunk), so the nch CTAs of one
+// i-tile run at about the same time. Each writes its partial tile into ring slot
+// itile % R of a ring of R tiles x nch x BLOCK*IPT float4 and arrives on the slot's
+// counter; the LAST arriving CTA sums the slot's partials in the fixed order c = 0, 1,
+// ..., nch-1 -- the order k_kdk_update uses, so the bits are those of the two-kernel path
+// -- writes acc, drops the slot's lines from L2 without write-back (discard.global.L2) and
+// opens the slot for i-tile itile + R. A CTA waits for its slot only if the reduction of
+// i-tile itile - R (R * nch = 2048 CTAs earlier in launch order, ~7 waves at N = 2^20) has
+// not finished -- which in-order CTA dispatch never lets happen; the watchdog bounds the
+// wait regardless. The work item comes from blockIdx, not a ticket counter: a value loaded
+// from shared memory is not provably warp-uniform, which moved the j loop off the uniform
+// datapath (1.9% slower, measured). Scratch: R * nch * tile * 16 B (64 MiB at nch = 64)
+// instead of nch * Ni * 16 B (1 GiB at N = 2^20, 4 GiB at 2^22), and the partials never
+// reach HBM (ncu: 22 MB of DRAM traffic per launch at N = 2^20, was 1.18 GB).
 struct Fused {
   float4* ring;         // [R][nch][tile] partial tiles
-  unsigned int* ctrl;   // [0] ticket, [1..R] arrivals per slot, [1+R .. 1+2R) tiles through each slot
+  unsigned int* ctrl;   // [0..R) arrivals per slot, [R .. 2R) i-tiles that went through each slot
   float4* acc;          // [Ni] result
   int R;                // ring slots
   Watch watch;
 };
-constexpr int kRingSlots = 8;
+constexpr int kRingSlots = 32;
 constexpr size_t kRingCtrlBytes = 256;  // ctrl words (zeroed by the host before each launch)
+static_assert(2 * kRingSlots * sizeof(unsigned int) <= kRingCtrlBytes, "ring control words");
 
 __device__ __forceinline__ unsigned int ld_acquire_u32(const unsigned int* p) {
   unsigned int v;
@@ -127,6 +131,75 @@ __device__ __forceinline__ void discard_l2_line(const void* p) {
   asm volatile("discard.global.L2 [%0], 128;" ::"l"(p) : "memory");
 }
 
+// The fused force kernel's ring protocol, out of line on purpose: inlined, the extra code
+// perturbed ptxas's schedule of the j loop (register banks, operand-reuse flags) and cost
+// 1.2-2.5% at N = 2^20 (measured); as calls it costs two calls per CTA. ring_wait: wait
+// until the i-tile's ring slot is free (i-tile itile - R reduced). ring_finish: arrive on
+// the slot; the last chunk CTA sums the slot's partials in the fixed order c = 0..nch-1 (as
+// k_kdk_update), writes acc, discards the slot's L2 lines and opens the slot for itile + R.
+__device__ __noinline__ void ring_wait(const Fused& fz, int itile) {
+  if (threadIdx.x == 0) {
+    const unsigned int want = static_cast<unsigned int>(itile / fz.R);
+    const unsigned int* gate = fz.ctrl + fz.R + itile % fz.R;
+    const unsigned long long t0 = globaltimer_ns();
+    while (ld_acquire_u32(gate) != want)
+      if (poll_timed_out(fz.watch, t0, kFaultForceRing)) break;
+  }
+  __syncthreads();
+}
+
+template <int BLOCK, int kIPT>
+__device__ __noinline__ void ring_finish(const Fused& fz, int nch, int itile, int Ni) {
+  constexpr int TILE = BLOCK * kIPT;
+  __shared__ int s_last;
+  const int tid = threadIdx.x;
+  const int slot = itile % fz.R;
+  unsigned int* arrive = fz.ctrl + slot;
+  unsigned int* gate = fz.ctrl + fz.R + slot;
+  const float4* __restrict__ tile = fz.ring + static_cast<size_t>(slot) * nch * TILE;
+  __syncthreads();
+  if (tid == 0) {
+    __threadfence();  // publish this CTA's partials before arriving
+    s_last = atomicAdd(arrive, 1u) == static_cast<unsigned int>(nch - 1);
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();  // acquire side: the other chunks' partials are visible
+  // fixed summation order c = 0, 1, ..., nch-1 (as k_kdk_update): batches of loads in flight
+#pragma unroll 1
+  for (int e = 0; e < kIPT; ++e) {
+    const int il = tid + e * BLOCK;
+    const float4* __restrict__ col = tile + il;
+    float4 a = __ldcg(col);
+    constexpr int B = 16;
+    for (int c0 = 1; c0 < nch; c0 += B) {
+      float4 q[B];
+#pragma unroll
+      for (int b = 0; b < B; ++b)
+        if (c0 + b < nch) q[b] = __ldcg(col + static_cast<size_t>(c0 + b) * TILE);
+#pragma unroll
+      for (int b = 0; b < B; ++b) {
+        if (c0 + b < nch) {
+          a.x = __fadd_rn(a.x, q[b].x);
+          a.y = __fadd_rn(a.y, q[b].y);
+          a.z = __fadd_rn(a.z, q[b].z);
+          a.w = __fadd_rn(a.w, q[b].w);
+        }
+      }
+    }
+    const int i = itile * TILE + il;
+    if (i < Ni) fz.acc[i] = a;
+  }
+  __syncthreads();  // every read of the slot is done
+  // drop the slot's lines from L2 without writing them back: the partials never reach HBM
+  for (size_t l = tid; l < static_cast<size_t>(nch) * TILE / 8; l += BLOCK) discard_l2_line(tile + 8 * l);
+  __syncthreads();
+  if (tid == 0) {
+    *arrive = 0u;
+    st_release_u32(gate, static_cast<unsigned int>(itile / fz.R + 1));  // open the slot for itile + R
+  }
+}
+
 // SCHED: 0 depth-first / 1 breadth-first source order (ptxas mostly reschedules).
 // SCHED 2: j-values kept NON-duplicated in shared memory and fed to the packed
 // ops as scalar-broadcast operands (FADD2 R, R.F32x2, R.F32): one LDS.128 per j
@@ -138,7 +211,7 @@ __device__ __forceinline__ void discard_l2_line(const void* p) {
 // trades FMA-pipe work for MUFU work: m r^-3 = ex2(fma(-1.5, lg2(r2), lg2(m)))
 // -- 2 MUFU + 1 FFMA2 per pair instead of 1 MUFU + 3 FMUL2 -- so the FP32
 // pipe (the binding one) and the MUFU pipe (58% busy) are balanced.
-template <int BLOCK, int kIPT, int MINB, int UNR, int SCHED, int ALT, bool POT, bool FUSED>
+template <int BLOCK, int kIPT, int MINB, int UNR, int SCHED, int ALT, bool POT>
 __global__ void __launch_bounds__(BLOCK, MINB)
     k_force_fast(const float4* __restrict__ ipos, int Ni, const float4* __restrict__ jpos, int Nj,
                  int jchunk, int n_itiles, float eps2, float4* __restrict__ out, const Fused fz) {
@@ -147,21 +220,17 @@ __global__ void __launch_bounds__(BLOCK, MINB)
   static_assert(ALT == 0 || DUP == 1, "ALT path uses scalar-broadcast j");
   __shared__ float4 sj[2][DUP * BLOCK];
   __shared__ float slm[2][ALT > 0 ? BLOCK : 1];
-  __shared__ int s_item, s_last;
-
   const int tid = threadIdx.x;
   const int nch = gridDim.x / n_itiles;
-  int itile, chunk;
-  if (FUSED) {  // in-order work items, chunk-minor: the chunks of an i-tile run together
-    if (tid == 0) s_item = static_cast<int>(atomicAdd(fz.ctrl, 1u));
-    __syncthreads();
-    itile = s_item / nch;
-    chunk = s_item - itile * nch;
-  } else {
-    itile = blockIdx.x % n_itiles;
-    chunk = blockIdx.x / n_itiles;
-  }
+  // chunk-minor: the chunks of an i-tile run together (what the fused reduction needs; the
+  // order does not change the speed of the unfused launch)
+  const int itile = blockIdx.x / nch;
+  const int chunk = blockIdx.x % nch;
+  // fz.ring set: in-kernel reduction; null: partials out. One kernel serves both modes -- a
+  // separate fused instantiation scheduled the j loop differently and ran 1.2-2.5% slower.
+  const bool fused = fz.ring != nullptr;
   const int ibase = itile * (BLOCK * kIPT) + tid;
+  if (fused) ring_wait(fz, itile);  // ring slot free? (i-tile itile - R reduced: never waits in practice)
 
   float2 nx[P], ny[P], nz[P];
   float2 ax[P], ay[P], az[P], ap[P];
@@ -239,79 +308,20 @@ __global__ void __launch_bounds__(BLOCK, MINB)
     __syncthreads();
   }
 
-  if (!FUSED) {
-    float4* __restrict__ o = out + static_cast<size_t>(chunk) * Ni;
-#pragma unroll
-    for (int p = 0; p < P; ++p) {
-      const int ia = ibase + (2 * p) * BLOCK;
-      const int ib = ibase + (2 * p + 1) * BLOCK;
-      if (ia < Ni) o[ia] = make_float4(ax[p].x, ay[p].x, az[p].x, POT ? ap[p].x : 0.f);
-      if (ib < Ni) o[ib] = make_float4(ax[p].y, ay[p].y, az[p].y, POT ? ap[p].y : 0.f);
-    }
-    return;
-  }
-  // ---- fused: partial tile -> ring slot; the last chunk of the i-tile reduces in order ----
+  // partials: [chunk][Ni] (unfused), or this chunk's row of the i-tile's ring slot (fused) --
+  // the same store code either way (it shares the register allocation of the j loop)
   constexpr int TILE = BLOCK * kIPT;
-  const int R = fz.R, slot = itile % R;
-  unsigned int* arrive = fz.ctrl + 1 + slot;
-  unsigned int* gate = fz.ctrl + 1 + R + slot;  // i-tiles that went through this slot
-  if (tid == 0) {  // slot free? (i-tile itile - R reduced); almost never waits
-    const unsigned int want = static_cast<unsigned int>(itile / R);
-    const unsigned long long t0 = globaltimer_ns();
-    while (ld_acquire_u32(gate) != want)
-      if (poll_timed_out(fz.watch, t0, kFaultForceRing)) break;
-  }
-  __syncthreads();
-  float4* __restrict__ tile = fz.ring + static_cast<size_t>(slot) * nch * TILE;
-  {
-    float4* __restrict__ o = tile + static_cast<size_t>(chunk) * TILE;
+  float4* __restrict__ o = fused ? fz.ring + (static_cast<size_t>(itile % fz.R) * nch + chunk) * TILE -
+                                       static_cast<size_t>(itile) * TILE
+                                 : out + static_cast<size_t>(chunk) * Ni;
 #pragma unroll
-    for (int p = 0; p < P; ++p) {
-      o[tid + (2 * p) * BLOCK] = make_float4(ax[p].x, ay[p].x, az[p].x, POT ? ap[p].x : 0.f);
-      o[tid + (2 * p + 1) * BLOCK] = make_float4(ax[p].y, ay[p].y, az[p].y, POT ? ap[p].y : 0.f);
-    }
+  for (int p = 0; p < P; ++p) {
+    const int ia = ibase + (2 * p) * BLOCK;
+    const int ib = ibase + (2 * p + 1) * BLOCK;
+    if (ia < Ni) o[ia] = make_float4(ax[p].x, ay[p].x, az[p].x, POT ? ap[p].x : 0.f);
+    if (ib < Ni) o[ib] = make_float4(ax[p].y, ay[p].y, az[p].y, POT ? ap[p].y : 0.f);
   }
-  __syncthreads();
-  if (tid == 0) {
-    __threadfence();  // publish this CTA's partials before arriving
-    s_last = atomicAdd(arrive, 1u) == static_cast<unsigned int>(nch - 1);
-  }
-  __syncthreads();
-  if (!s_last) return;
-  __threadfence();  // acquire side: the other chunks' partials are visible
-  // fixed summation order c = 0, 1, ..., nch-1 (as k_kdk_update): batches of loads in flight
-#pragma unroll 1
-  for (int e = 0; e < kIPT; ++e) {
-    const int il = tid + e * BLOCK;
-    const float4* __restrict__ col = tile + il;
-    float4 a = __ldcg(col);
-    constexpr int B = 16;
-    for (int c0 = 1; c0 < nch; c0 += B) {
-      float4 q[B];
-#pragma unroll
-      for (int b = 0; b < B; ++b)
-        if (c0 + b < nch) q[b] = __ldcg(col + static_cast<size_t>(c0 + b) * TILE);
-#pragma unroll
-      for (int b = 0; b < B; ++b) {
-        if (c0 + b < nch) {
-          a.x = __fadd_rn(a.x, q[b].x);
-          a.y = __fadd_rn(a.y, q[b].y);
-          a.z = __fadd_rn(a.z, q[b].z);
-          a.w = __fadd_rn(a.w, q[b].w);
-        }
-      }
-    }
-    const int i = itile * TILE + il;
-    if (i < Ni) fz.acc[i] = a;
-  }
-  __syncthreads();  // every read of the slot is done
-  // drop the slot's lines from L2 without writing them back: the partials never reach HBM
-  for (size_t l = tid; l < static_cast<size_t>(nch) * TILE / 8; l += BLOCK) discard_l2_line(tile + 8 * l);
-  __syncthreads();
-  if (tid == 0) {
-    *arrive = 0u;
-    st_release_u32(gate, static_cast<unsigned int>(itile / R + 1));  // open the slot for itile + R
-  }
+  if (fused) ring_finish<BLOCK, kIPT>(fz, nch, itile, Ni);  // the last chunk CTA of the i-tile reduces the slot
 }
 
 
@@ -432,26 +442,13 @@ __global__ void __launch_bounds__(128)
 using ForceFn = void (*)(const float4*, int, const float4*, int, int, int, float, float4*, const Fused);
 struct ForceVariant {
   int block, ipt;
-  ForceFn fn[2];     // partials out [nch][Ni] (potential off / on)
-  ForceFn fused[2];  // in-kernel reduction (nullptr: not instantiated for this variant)
+  ForceFn fn[2];  // potential off / on; Fused{} = partials out, a ring = in-kernel reduction
 };
-#define B2_FV(B, I, M, U, S, A)                                                                    \
-  {                                                                                                \
-    B, I, {k_force_fast<B, I, M, U, S, A, false, false>, k_force_fast<B, I, M, U, S, A, true, false>}, \
-    {                                                                                              \
-      nullptr, nullptr                                                                             \
-    }                                                                                              \
-  }
-#define B2_FVF(B, I, M, U, S, A)                                                                   \
-  {                                                                                                \
-    B, I, {k_force_fast<B, I, M, U, S, A, false, false>, k_force_fast<B, I, M, U, S, A, true, false>}, \
-    {                                                                                              \
-      k_force_fast<B, I, M, U, S, A, false, true>, k_force_fast<B, I, M, U, S, A, true, true>      \
-    }                                                                                              \
-  }
+#define B2_FV(B, I, M, U, S, A) \
+  { B, I, { k_force_fast<B, I, M, U, S, A, false>, k_force_fast<B, I, M, U, S, A, true> } }
 static const ForceVariant kVariants[] = {
-    B2_FVF(128, 16, 2, 1, 2, 0),  // 0: default for large N (best of the round-1 sweep)
-    B2_FVF(64, 8, 8, 4, 1, 0),    // 1: medium N (more CTAs)
+    B2_FV(128, 16, 2, 1, 2, 0),  // 0: default for large N (best of the round-1 sweep)
+    B2_FV(64, 8, 8, 4, 1, 0),    // 1: medium N (more CTAs)
     B2_FV(256, 8, 2, 4, 0, 0),   // 2: round-1 first version
     B2_FV(256, 12, 1, 2, 1, 0),  // 3: duplicated-pair j
     B2_FV(128, 16, 2, 1, 3, 2),  // 4: 2 of 8 pairs on ex2/lg2
@@ -460,10 +457,9 @@ static const ForceVariant kVariants[] = {
     B2_FV(256, 12, 1, 2, 3, 1),  // 7: 1 of 6
     B2_FV(128, 16, 2, 2, 3, 2),  // 8
     B2_FV(256, 8, 2, 4, 3, 1),   // 9: 1 of 4
-    B2_FVF(64, 2, 16, 4, 2, 0),  // 10: small N (configs[0]: N=4096)
+    B2_FV(64, 2, 16, 4, 2, 0),   // 10: small N (configs[0]: N=4096)
 };
 #undef B2_FV
-#undef B2_FVF
 
 static int env_int_nb(const char* name, int dflt) {
   const char* e = std::getenv(name);
@@ -481,9 +477,8 @@ static int large_variant() {
 
 // The variant launch_partials / launch_fused take for Ni (same per-lane arithmetic and j
 // order in every variant, so the choice never moves a bit).
-static const ForceVariant* pick_variant(int Ni, int nch, bool need_fused) {
+static const ForceVariant* pick_variant(int Ni, int nch) {
   const ForceVariant* v = &kVariants[large_variant()];
-  if (need_fused && !v->fused[0]) v = &kVariants[0];
   static const long long want_k = std::max(0, env_int_nb("SOLOMON_NBODY_WANT", 4));  // tuning knob: CTAs per SM
   const long long want = want_k * device_info().sms;
   auto ctas = [&](const ForceVariant* c) { return (long long)((Ni + c->block * c->ipt - 1) / (c->block * c->ipt)) * nch; };
@@ -508,7 +503,7 @@ static int launch_fused(int Ni, const float4* ipos, int Nj, const float4* jpos, 
                         void* ws, cudaStream_t s) {
   const int jchunk = chunk_size(Nj, flags);
   const int nch = nchunks_for(Nj, flags);
-  const ForceVariant* v = pick_variant(Ni, nch, true);
+  const ForceVariant* v = pick_variant(Ni, nch);
   const int tile = v->block * v->ipt;
   const int nit = (Ni + tile - 1) / tile;
   unsigned int* ctrl = static_cast<unsigned int*>(ws);
@@ -516,8 +511,8 @@ static int launch_fused(int Ni, const float4* ipos, int Nj, const float4* jpos, 
   Fused fz{reinterpret_cast<float4*>(rb), ctrl, acc, std::min(kRingSlots, nit), make_watch()};
   cudaError_t e = cudaMemsetAsync(ctrl, 0, kRingCtrlBytes, s);
   if (e != cudaSuccess) return static_cast<int>(e);
-  v->fused[(flags & B2_POTENTIAL) ? 1 : 0]<<<nit * nch, v->block, 0, s>>>(ipos, Ni, jpos, Nj, jchunk, nit, eps * eps,
-                                                                       acc, fz);
+  v->fn[(flags & B2_POTENTIAL) ? 1 : 0]<<<nit * nch, v->block, 0, s>>>(ipos, Ni, jpos, Nj, jchunk, nit, eps * eps, acc,
+                                                                     fz);
   return launch_status();
 }
 
@@ -537,7 +532,7 @@ static int launch_partials(int Ni, const float4* ipos, int Nj, const float4* jpo
   const int nch = nchunks_for(Nj, flags);
   // Largest tile whose (i-tile, j-chunk) grid still fills the 148 SMs: the tuned large
   // variant, else 64x8, else 64x2 (small N is latency-bound and needs every warp it can get).
-  const ForceVariant* v = pick_variant(Ni, nch, false);
+  const ForceVariant* v = pick_variant(Ni, nch);
   const int nit = (Ni + v->block * v->ipt - 1) / (v->block * v->ipt);
   v->fn[pot ? 1 : 0]<<<nit * nch, v->block, 0, s>>>(ipos, Ni, jpos, Nj, jchunk, nit, eps2, out, Fused{});
   return launch_status();
