@@ -1083,6 +1083,9 @@ def run_parity_configs(dev):
     lf = b2.Leapfrog(torch.from_numpy(pos).to(dev), torch.from_numpy(vel).to(dev), eps, dt)
     torch.cuda.synchronize(dev)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    # device time of the run: a ~50 us spin queued first keeps the host's launch latency out of
+    # the events (the run is one memset + one launch)
+    torch.cuda._sleep(100_000)
     e0.record()
     lf.step(steps)
     e1.record()

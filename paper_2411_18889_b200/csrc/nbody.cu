@@ -457,7 +457,8 @@ static const ForceVariant kVariants[] = {
     B2_FV(256, 12, 1, 2, 3, 1),  // 7: 1 of 6
     B2_FV(128, 16, 2, 2, 3, 2),  // 8
     B2_FV(256, 8, 2, 4, 3, 1),   // 9: 1 of 4
-    B2_FV(64, 2, 16, 4, 2, 0),   // 10: small N (configs[0]: N=4096)
+    B2_FV(64, 2, 16, 4, 2, 0),   // 10: small N
+    B2_FV(32, 2, 32, 4, 2, 0),   // 11: 32-j chunks (Nj <= kFineChunkNj, e.g. configs[0]: N=4096)
 };
 #undef B2_FV
 
@@ -477,7 +478,8 @@ static int large_variant() {
 
 // The variant launch_partials / launch_fused take for Ni (same per-lane arithmetic and j
 // order in every variant, so the choice never moves a bit).
-static const ForceVariant* pick_variant(int Ni, int nch) {
+static const ForceVariant* pick_variant(int Ni, int nch, int jchunk) {
+  if (jchunk < 64) return &kVariants[11];  // a j tile never spans two chunks' worth of padding
   const ForceVariant* v = &kVariants[large_variant()];
   static const long long want_k = std::max(0, env_int_nb("SOLOMON_NBODY_WANT", 4));  // tuning knob: CTAs per SM
   const long long want = want_k * device_info().sms;
@@ -503,7 +505,7 @@ static int launch_fused(int Ni, const float4* ipos, int Nj, const float4* jpos, 
                         void* ws, cudaStream_t s) {
   const int jchunk = chunk_size(Nj, flags);
   const int nch = nchunks_for(Nj, flags);
-  const ForceVariant* v = pick_variant(Ni, nch);
+  const ForceVariant* v = pick_variant(Ni, nch, jchunk);
   const int tile = v->block * v->ipt;
   const int nit = (Ni + tile - 1) / tile;
   unsigned int* ctrl = static_cast<unsigned int*>(ws);
@@ -532,7 +534,7 @@ static int launch_partials(int Ni, const float4* ipos, int Nj, const float4* jpo
   const int nch = nchunks_for(Nj, flags);
   // Largest tile whose (i-tile, j-chunk) grid still fills the 148 SMs: the tuned large
   // variant, else 64x8, else 64x2 (small N is latency-bound and needs every warp it can get).
-  const ForceVariant* v = pick_variant(Ni, nch);
+  const ForceVariant* v = pick_variant(Ni, nch, jchunk);
   const int nit = (Ni + v->block * v->ipt - 1) / (v->block * v->ipt);
   v->fn[pot ? 1 : 0]<<<nit * nch, v->block, 0, s>>>(ipos, Ni, jpos, Nj, jchunk, nit, eps2, out, Fused{});
   return launch_status();
@@ -648,8 +650,8 @@ int b2_kdk_update_publish(int n, const float* pos_in, float* pos_out, float* vel
 
 size_t b2_leapfrog_workspace_bytes(int n, int flags) {
   const int ff = flags & (B2_POTENTIAL | B2_EXACT);
-  // the fused force's ring, or the persistent small-N path's [2][n] position words
-  return std::max(b2_calc_acc_workspace_bytes(n, n, ff), 2 * static_cast<size_t>(std::max(n, 0)) * sizeof(uint4));
+  // the fused force's ring, or the persistent small-N path's [2][n] position words + ready lines
+  return std::max(b2_calc_acc_workspace_bytes(n, n, ff), small_workspace_bytes(n));
 }
 
 int b2_leapfrog(int n, float* pos, float* vel, float* acc, float eps, float dt, int nsteps, int flags,

@@ -79,11 +79,20 @@ __device__ __forceinline__ void interact_bf(const float2 X, const float2 Y, cons
   }
 }
 
+// j-chunk size, a function of Nj only (so sharded and unsharded runs sum in the same
+// order). Large Nj: ~64 chunks, 64-aligned (the tile kernel's waves and ring). Nj up to
+// kFineChunkNj: ~128 chunks, 32-aligned -- the persistent small-N leapfrog's parallelism
+// is (own particles / 2) x chunks per SM, and 128 chunks give it 8 warps x 7 packed pairs
+// at N = 4096 (64 chunks left it at 14 warps x 2 pairs, ~55% of the FMA pipe).
+constexpr int kFineChunkNj = 6144;
+constexpr int kFineChunks = 128, kFineAlign = 32;
 inline int chunk_size(int Nj, int flags) {
   if (flags & B2_EXACT) return Nj;
-  int c = (Nj + kTargetChunks - 1) / kTargetChunks;
-  c = (c + kChunkAlign - 1) / kChunkAlign * kChunkAlign;
-  return std::max(c, kChunkAlign);
+  const int target = Nj <= kFineChunkNj ? kFineChunks : kTargetChunks;
+  const int align = Nj <= kFineChunkNj ? kFineAlign : kChunkAlign;
+  int c = (Nj + target - 1) / target;
+  c = (c + align - 1) / align * align;
+  return std::max(c, align);
 }
 
 inline int nchunks_for(int Nj, int flags) {
@@ -94,6 +103,7 @@ inline int nchunks_for(int Nj, int flags) {
 
 // The persistent small-N path of b2_leapfrog (nbody_small.cu); false = not applicable,
 // nothing launched.
+size_t small_workspace_bytes(int n);
 bool launch_leapfrog_small(int n, float4* pos, float4* vel, float4* acc, float eps, float dt, int nsteps, int flags,
                            void* workspace, size_t workspace_bytes, cudaStream_t s);
 
