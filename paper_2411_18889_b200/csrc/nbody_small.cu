@@ -44,6 +44,10 @@ namespace b2 {
 // with the same packed-FP32 interaction, partials summed c = 0, 1, ... and the
 // same FMA kick/drift sequence.
 constexpr int kSmallMaxThreads = 256;
+#ifndef B2_SMALL_UNROLL
+#define B2_SMALL_UNROLL 2
+#endif
+constexpr int kSmallUnroll = B2_SMALL_UNROLL;  // j-loop unroll of the force task
 constexpr int kSmallImax = 32;   // own particles per CTA (at most; even)
 constexpr int kSmallMaxNP = 8;   // packed pairs per thread
 
@@ -151,7 +155,7 @@ __global__ void __launch_bounds__(kSmallMaxThreads, 1) k_leapfrog_small(const Sm
     const float4* q = P + c * (chunk + 1);
     const int len = min(chunk, n - c * chunk);
 #ifndef B2_SMALL_PREFETCH
-#define B2_SMALL_PREFETCH 1
+#define B2_SMALL_PREFETCH 0  // 1: next j loaded one iteration ahead (measured slower: 7.15 vs 6.95 us)
 #endif
 #if B2_SMALL_PREFETCH
     float4 pj = *q++;
@@ -165,7 +169,7 @@ __global__ void __launch_bounds__(kSmallMaxThreads, 1) k_leapfrog_small(const Sm
     }
 #else
     const float4* const qend = q + len;
-#pragma unroll 1
+#pragma unroll kSmallUnroll
     for (; q != qend; ++q) {
       const float4 pj = *q;
       interact_bf<NP, POT>(make_float2(pj.x, pj.x), make_float2(pj.y, pj.y), make_float2(pj.z, pj.z),
@@ -253,16 +257,43 @@ __global__ void __launch_bounds__(kSmallMaxThreads, 1) k_leapfrog_small(const Sm
   };
   // warp 0 after its lanes t < I published: one arrival on counter blockIdx % 8 (release: the
   // words are visible to whoever acquires the count)
+#ifndef B2_SMALL_WARPSYNC
+#define B2_SMALL_WARPSYNC 1
+#endif
+  // counter of CTA b: b % 8 (step-wide wait), or the contiguous group b * 8 / ctas (per-warp wait)
+  auto counter_of = [&](int b) { return B2_SMALL_WARPSYNC ? b * 8 / static_cast<int>(gridDim.x) : b & 7; };
+  auto counter_size = [&](int k) {  // CTAs on counter k
+    const int C = gridDim.x;
+    return B2_SMALL_WARPSYNC ? ((k + 1) * C + 7) / 8 - (k * C + 7) / 8 : (C - k + 7) / 8;
+  };
   auto announce = [&]() {
     __syncwarp();
-    if (tid == 0) red_release_add_u32(a.arrive + 32 * (blockIdx.x & 7), 1u);
+    if (tid == 0) red_release_add_u32(a.arrive + 32 * counter_of(blockIdx.x), 1u);
+  };
+  // this warp: wait until the CTAs on the counters of its slice's producers published `state`
+  auto slice_published = [&](int state) -> bool {
+    bool ok = true;
+    if (wc0 < wc1) {
+      const int k0 = counter_of(wj0 / IB), k1 = counter_of((wj1 - 1) / IB);
+      if (lane <= k1 - k0) {
+        const int k = k0 + lane;
+        const unsigned int want = static_cast<unsigned int>(counter_size(k)) * state;
+        const unsigned long long t0 = globaltimer_ns();
+        for (unsigned int it = 1; ld_acquire_u32_gpu(a.arrive + 32 * k) < want; ++it)
+          if (!(it & 31) && poll_expired(a.watch, t0, kFaultLeapfrogSmall)) {
+            ok = false;
+            break;
+          }
+      }
+    }
+    return __all_sync(0xffffffffu, ok);
   };
   // warp 0: wait until every CTA published state `state` (lane k < 8 acquires counter k);
   // false = the watchdog gave up
   auto all_published = [&](int state) -> bool {
     bool ok = true;
     if (lane < 8) {
-      const unsigned int want = static_cast<unsigned int>((gridDim.x - lane + 7) / 8) * state;
+      const unsigned int want = static_cast<unsigned int>(counter_size(lane)) * state;
       const unsigned long long t0 = globaltimer_ns();
       // the watchdog every 32nd poll: its own load would double each poll's round trip
       for (unsigned int k = 1; ld_acquire_u32_gpu(a.arrive + 32 * lane) < want; ++k)
@@ -306,6 +337,18 @@ __global__ void __launch_bounds__(kSmallMaxThreads, 1) k_leapfrog_small(const Sm
       // every CTA published state st+1 (barrier + CTA-wide vote: no static shared memory, the
       // dynamic allocation may use it all); a watchdog expiry leaves without writing pos / vel /
       // acc (b2_fault_status reports it)
+#if B2_SMALL_WARPSYNC
+      const bool ok = slice_published(st + 1);
+      B2_STRACE(1);
+      B2_WTRACE(8);
+      if (ok) {
+        fetch_slice(st + 1, st);
+        B2_WTRACE(16);
+        force_task();
+      }
+      B2_WTRACE(24);
+      if (__syncthreads_or(!ok)) return;
+#else
       if (__syncthreads_or(tid < 32 && !all_published(st + 1))) return;
       B2_STRACE(1);
       B2_WTRACE(8);
@@ -314,6 +357,7 @@ __global__ void __launch_bounds__(kSmallMaxThreads, 1) k_leapfrog_small(const Sm
       force_task();
       B2_WTRACE(24);
       __syncthreads();
+#endif
       B2_STRACE(2);
       reduce_all();
       B2_STRACE(3);
