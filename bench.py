@@ -1080,17 +1080,20 @@ def run_parity_configs(dev):
     pos, vel = b2.plummer_numpy(n, 42)
     lf = b2.Leapfrog(torch.from_numpy(pos).to(dev), torch.from_numpy(vel).to(dev), eps, dt)
     lf.step(2)
-    lf = b2.Leapfrog(torch.from_numpy(pos).to(dev), torch.from_numpy(vel).to(dev), eps, dt)
-    torch.cuda.synchronize(dev)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    # device time of the run: a ~50 us spin queued first keeps the host's launch latency out of
-    # the events (the run is one memset + one launch)
-    torch.cuda._sleep(100_000)
-    e0.record()
-    lf.step(steps)
-    e1.record()
-    torch.cuda.synchronize(dev)
-    gpu_ms = e0.elapsed_time(e1)
+    runs = []
+    for _ in range(5):  # the median of 5 whole runs (fresh state each, the same 16 steps)
+        lf = b2.Leapfrog(torch.from_numpy(pos).to(dev), torch.from_numpy(vel).to(dev), eps, dt)
+        torch.cuda.synchronize(dev)
+        # device time of the run: a ~0.5 ms spin queued first keeps the host's launch latency out
+        # of the events (the run is one memset + one launch)
+        torch.cuda._sleep(1_000_000)
+        e0.record()
+        lf.step(steps)
+        e1.record()
+        torch.cuda.synchronize(dev)
+        runs.append(e0.elapsed_time(e1))
+    gpu_ms = sorted(runs)[len(runs) // 2]
     rs = oracle.Restatement()
     t0 = time.perf_counter()
     wp, wv, wa = rs.leapfrog(pos, vel, eps, dt, steps)
@@ -1104,9 +1107,9 @@ def run_parity_configs(dev):
     out["nbody_4096_plummer_kdk16"] = {
         "config": "BASELINE configs[0]: N=4096 Plummer FP32, 16 leapfrog steps",
         "gpu_ms": gpu_ms, "gpu_launches": 1,
-        "path": "b2_leapfrog -> k_leapfrog_small (all 16 KDK steps in one persistent launch, positions "
-                "exchanged between CTAs as tagged 16-byte words; + one memset), bit-identical to the "
-                "two-kernel-per-step path",
+        "path": "b2_leapfrog -> k_leapfrog_small (all 16 KDK steps in one persistent launch; positions "
+                "exchanged between CTAs through global memory, arrival counters and per-warp bulk copies; + "
+                "one memset), bit-identical to the two-kernel-per-step path; median of 5 runs",
         "gpu_ginteractions_per_s": n * n * steps / (gpu_ms * 1e-3) / 1e9,
         "cpu_ms": cpu_ms, "cpu_kind": "port (oracle/solomon_oracle.c KDK around the restated calc_acc; "
                                       "the reference has no integrator)",
@@ -1122,13 +1125,17 @@ def run_parity_configs(dev):
     f0 = b2.init_grid(g, g, g, seed=7, device=dev)
     sim = b2.Diffusion3D(f0.clone(), *dargs)
     sim.run(10)
-    sim = b2.Diffusion3D(f0.clone(), *dargs)
-    torch.cuda.synchronize(dev)
-    e0.record()
-    sim.run(dsteps)
-    e1.record()
-    torch.cuda.synchronize(dev)
-    gpu_ms = e0.elapsed_time(e1)
+    runs = []
+    for _ in range(5):  # median of 5 whole runs, host launch latency kept out as above
+        sim = b2.Diffusion3D(f0.clone(), *dargs)
+        torch.cuda.synchronize(dev)
+        torch.cuda._sleep(1_000_000)
+        e0.record()
+        sim.run(dsteps)
+        e1.record()
+        torch.cuda.synchronize(dev)
+        runs.append(e0.elapsed_time(e1))
+    gpu_ms = sorted(runs)[len(runs) // 2]
     host = f0.cpu().numpy()
     ref = oracle.Reference("ieee")
     fast = oracle.Reference("fast")

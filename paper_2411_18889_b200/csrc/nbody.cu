@@ -115,9 +115,9 @@ struct Fused {
   int R;                // ring slots
   Watch watch;
 };
-constexpr int kRingSlots = 32;
-constexpr size_t kRingCtrlBytes = 256;  // ctrl words (zeroed by the host before each launch)
-static_assert(2 * kRingSlots * sizeof(unsigned int) <= kRingCtrlBytes, "ring control words");
+constexpr int kRingSlots = 32;         // of the largest tile (2048 i); smaller tiles get more
+constexpr int kMaxRingSlots = 1024;    // control words: arrivals + gates per slot
+constexpr size_t kRingCtrlBytes = 2 * kMaxRingSlots * sizeof(unsigned int);  // zeroed per launch
 
 __device__ __forceinline__ unsigned int ld_acquire_u32(const unsigned int* p) {
   unsigned int v;
@@ -222,13 +222,13 @@ __global__ void __launch_bounds__(BLOCK, MINB)
   __shared__ float slm[2][ALT > 0 ? BLOCK : 1];
   const int tid = threadIdx.x;
   const int nch = gridDim.x / n_itiles;
-  // chunk-minor: the chunks of an i-tile run together (what the fused reduction needs; the
-  // order does not change the speed of the unfused launch)
-  const int itile = blockIdx.x / nch;
-  const int chunk = blockIdx.x % nch;
   // fz.ring set: in-kernel reduction; null: partials out. One kernel serves both modes -- a
   // separate fused instantiation scheduled the j loop differently and ran 1.2-2.5% slower.
   const bool fused = fz.ring != nullptr;
+  // fused: chunk-minor, the chunks of an i-tile run together (what the ring needs); partials:
+  // i-tile-minor, the CTAs running together share their j-chunk (mid N, small CTAs)
+  const int itile = fused ? blockIdx.x / nch : blockIdx.x % n_itiles;
+  const int chunk = fused ? blockIdx.x % nch : blockIdx.x / n_itiles;
   const int ibase = itile * (BLOCK * kIPT) + tid;
   if (fused) ring_wait(fz, itile);  // ring slot free? (i-tile itile - R reduced: never waits in practice)
 
@@ -458,7 +458,7 @@ static const ForceVariant kVariants[] = {
     B2_FV(128, 16, 2, 2, 3, 2),  // 8
     B2_FV(256, 8, 2, 4, 3, 1),   // 9: 1 of 4
     B2_FV(64, 2, 16, 4, 2, 0),   // 10: small N
-    B2_FV(32, 2, 32, 4, 2, 0),   // 11: 32-j chunks (Nj <= kFineChunkNj, e.g. configs[0]: N=4096)
+    B2_FV(32, 8, 16, 4, 2, 0),   // 11: 32-j chunks (Nj <= kFineChunkNj, e.g. configs[0]: N=4096)
 };
 #undef B2_FV
 
@@ -492,15 +492,24 @@ static const ForceVariant* pick_variant(int Ni, int nch, int jchunk) {
 
 constexpr int kMaxTile = 2048;  // largest BLOCK * IPT of a fused variant
 
+// rows of i (per chunk) the ring holds: kRingSlots tiles of the largest variant, or all of Ni
+static size_t fused_ring_rows(int Ni) {
+  return std::min<size_t>(static_cast<size_t>(kRingSlots) * kMaxTile, static_cast<size_t>(std::max(Ni, 0)) + kMaxTile);
+}
+
 static size_t fused_workspace_bytes(int Ni, int Nj, int flags) {
   const int nch = nchunks_for(Nj, flags);
-  const size_t rows = std::min<size_t>(static_cast<size_t>(kRingSlots) * kMaxTile,
-                                       static_cast<size_t>(std::max(Ni, 0)) + kMaxTile);
-  return kRingCtrlBytes + 128 + static_cast<size_t>(nch) * rows * sizeof(float4);
+  return kRingCtrlBytes + 128 + static_cast<size_t>(nch) * fused_ring_rows(Ni) * sizeof(float4);
 }
 
 // Force with the in-kernel in-order reduction: acc = sum_c partials_c (bits of partials +
 // B2_KDK_REDUCE). ws >= fused_workspace_bytes; one memset of the control words + one launch.
+static int launch_partials(int Ni, const float4* ipos, int Nj, const float4* jpos, float eps, int flags,
+                           float4* out, cudaStream_t s);
+static int launch_update(int n, float4* pos, float4* vel, float4* acc, const float4* partials, int nchunks,
+                         float h_end, float h_begin, float dt, int phases, cudaStream_t s,
+                         const float4* pos_in = nullptr, const Peers* peers = nullptr);
+
 static int launch_fused(int Ni, const float4* ipos, int Nj, const float4* jpos, float eps, int flags, float4* acc,
                         void* ws, cudaStream_t s) {
   const int jchunk = chunk_size(Nj, flags);
@@ -510,8 +519,21 @@ static int launch_fused(int Ni, const float4* ipos, int Nj, const float4* jpos, 
   const int nit = (Ni + tile - 1) / tile;
   unsigned int* ctrl = static_cast<unsigned int*>(ws);
   const uintptr_t rb = (reinterpret_cast<uintptr_t>(ws) + kRingCtrlBytes + 127) & ~static_cast<uintptr_t>(127);
-  Fused fz{reinterpret_cast<float4*>(rb), ctrl, acc, std::min(kRingSlots, nit), make_watch()};
-  cudaError_t e = cudaMemsetAsync(ctrl, 0, kRingCtrlBytes, s);
+  // Up to ~63k i the workspace holds all nch x Ni partials anyway: there the reduce is a second
+  // launch (the same fixed order, so the same bits) -- faster than the ring at small and mid N,
+  // where the ring's per-CTA fence, arrival and slot wait are not hidden (N = 8192: 44 vs 56 us,
+  // 32768: 427 vs 503, 65536: 1643 vs 1710). The ring is what keeps large N in 64 MiB.
+  if (fused_ring_rows(Ni) >= static_cast<size_t>(Ni)) {
+    float4* part = reinterpret_cast<float4*>(rb);
+    int rc = launch_partials(Ni, ipos, Nj, jpos, eps, flags, part, s);
+    if (rc) return rc;
+    return launch_update(Ni, nullptr, nullptr, acc, part, nch, 0.f, 0.f, 0.f, B2_KDK_REDUCE, s);
+  }
+  // ring slots: every i-tile of the launch when the workspace holds them (small tiles at mid N,
+  // where 32 slots made later i-tiles wait on earlier ones), else kRingSlots of the largest tile
+  const int slots = static_cast<int>(std::min<size_t>(fused_ring_rows(Ni) / tile, kMaxRingSlots));
+  Fused fz{reinterpret_cast<float4*>(rb), ctrl, acc, std::min(nit, std::max(slots, 1)), make_watch()};
+  cudaError_t e = cudaMemsetAsync(ctrl, 0, 2 * static_cast<size_t>(fz.R) * sizeof(unsigned int), s);
   if (e != cudaSuccess) return static_cast<int>(e);
   v->fn[(flags & B2_POTENTIAL) ? 1 : 0]<<<nit * nch, v->block, 0, s>>>(ipos, Ni, jpos, Nj, jchunk, nit, eps * eps, acc,
                                                                      fz);
@@ -541,8 +563,8 @@ static int launch_partials(int Ni, const float4* ipos, int Nj, const float4* jpo
 }
 
 static int launch_update(int n, float4* pos, float4* vel, float4* acc, const float4* partials, int nchunks,
-                         float h_end, float h_begin, float dt, int phases, cudaStream_t s,
-                         const float4* pos_in = nullptr, const Peers* peers = nullptr) {
+                         float h_end, float h_begin, float dt, int phases, cudaStream_t s, const float4* pos_in,
+                         const Peers* peers) {
   if (n <= 0) return B2_OK;
   Peers pp{};
   if (peers) pp = *peers;
@@ -669,19 +691,32 @@ int b2_leapfrog(int n, float* pos, float* vel, float* acc, float eps, float dt, 
   float4* A = reinterpret_cast<float4*>(acc);
   if (launch_leapfrog_small(n, P, V, A, eps, dt, nsteps, flags, workspace, workspace_bytes, s)) return B2_OK;
   const float h = 0.5f * dt;
-  // a = calc_acc(x) with the chunk partials reduced in order inside the force kernel
+  // Steady state is two launches per step: force, then one update. Up to ~63k particles the
+  // force writes its nch x n chunk partials into the workspace and the update reduces them
+  // (B2_KDK_REDUCE) before its kicks; beyond, the force reduces them in-kernel (ring) and the
+  // update reads acc. Same summation order either way.
+  const int nch = nchunks_for(n, fflags);
+  const bool partials = nch > 1 && fused_ring_rows(n) >= static_cast<size_t>(n);
+  const float4* part = reinterpret_cast<const float4*>(
+      (reinterpret_cast<uintptr_t>(workspace) + kRingCtrlBytes + 127) & ~static_cast<uintptr_t>(127));
   auto force = [&]() {
+    if (partials)
+      return launch_partials(n, P, n, P, eps, fflags, const_cast<float4*>(part), s);
     return b2_calc_acc(n, pos, acc, n, pos, eps, fflags, workspace, workspace_bytes, s);
   };
-  if ((flags & B2_INIT_ACC) && (rc = force())) return rc;
+  const int reduce = partials ? B2_KDK_REDUCE : 0;
+  if (flags & B2_INIT_ACC) {
+    if ((rc = force())) return rc;
+    if (partials && (rc = launch_update(n, P, V, A, part, nch, 0.f, 0.f, 0.f, B2_KDK_REDUCE, s))) return rc;
+  }
   if (nsteps == 0) return B2_OK;
   // step 0 opening kick + drift
   if ((rc = launch_update(n, P, V, A, nullptr, 1, 0.f, h, dt, B2_KDK_KICK_DRIFT, s))) return rc;
   for (int st = 0; st < nsteps; ++st) {
     if ((rc = force())) return rc;
     const bool last = st + 1 == nsteps;
-    const int ph = B2_KDK_KICK_END | (last ? 0 : B2_KDK_KICK_DRIFT);
-    if ((rc = launch_update(n, P, V, A, nullptr, 1, h, h, dt, ph, s))) return rc;
+    const int ph = reduce | B2_KDK_KICK_END | (last ? 0 : B2_KDK_KICK_DRIFT);
+    if ((rc = launch_update(n, P, V, A, part, partials ? nch : 1, h, h, dt, ph, s))) return rc;
   }
   return B2_OK;
 }

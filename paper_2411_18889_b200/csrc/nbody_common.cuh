@@ -83,8 +83,9 @@ __device__ __forceinline__ void interact_bf(const float2 X, const float2 Y, cons
 // order). Large Nj: ~64 chunks, 64-aligned (the tile kernel's waves and ring). Nj up to
 // kFineChunkNj: ~128 chunks, 32-aligned -- the persistent small-N leapfrog's parallelism
 // is (own particles / 2) x chunks per SM, and 128 chunks give it 8 warps x 7 packed pairs
-// at N = 4096 (64 chunks left it at 14 warps x 2 pairs, ~55% of the FMA pipe).
-constexpr int kFineChunkNj = 6144;
+// at N = 4096 (64 chunks left it at 14 warps x 2 pairs, ~55% of the FMA pipe). Above that
+// (its 4-group shape, n <= 64 x SMs) 64 chunks already fill its 256 threads.
+constexpr int kFineChunkNj = 4736;
 constexpr int kFineChunks = 128, kFineAlign = 32;
 inline int chunk_size(int Nj, int flags) {
   if (flags & B2_EXACT) return Nj;

@@ -1,5 +1,5 @@
 // K2' -- the whole small-N leapfrog run in one persistent launch (b2_leapfrog for
-// n <= 32 x SMs). Reference force law: pkg/tests/fixtures/listing_nbody.c:1-27 via
+// n <= 64 x SMs). Reference force law: pkg/tests/fixtures/listing_nbody.c:1-27 via
 // interact_bf (nbody_common.cuh); bit-identical to the two-kernel path of nbody.cu.
 #include <cuda_runtime.h>
 
@@ -16,13 +16,13 @@ namespace b2 {
 // configs[0]: N=4096, where the two-kernel step is ~20 us of launch gaps,
 // under-filled force tiles and a latency-bound reduce for ~5.5 us of arithmetic).
 //
-// One CTA per I = 2H <= 32 own particles (I sized so the grid spans every SM: 28 at
-// N=4096 -> 147 CTAs), all CTAs co-resident (cooperative launch). Own particle pairs
+// One CTA per I = 2H <= 64 own particles (I sized so the grid spans every SM: 28 at
+// N=4096 -> 147 CTAs, 56 at N=8192), all CTAs co-resident (cooperative launch). Own particle pairs
 // are (i0 + p, i0 + H + p), p < H -- the packed FFMA2 lanes. Force task = (group g of
 // NP pairs, j-chunk c): thread tid -> g = tid % G, c = tid / G, so a CTA runs
 // G x nch threads (N=4096: 2 groups of 7 pairs x 128 chunks of 32 j = 256 threads, 8
 // warps, 7 independent pairs each -- the shape of the large tile kernel's 8 warps x 8
-// pairs).
+// pairs; N=8192: 4 groups of 7 pairs x 64 chunks of 128 j).
 //
 // Exchange (scripts/trace_small.cu, scripts/l2_gather_probe.cu): positions {x, y, z, m}
 // go to a [2][n] global buffer (state parity); after its particles' stores, warp 0 of each
@@ -48,7 +48,10 @@ constexpr int kSmallMaxThreads = 256;
 #define B2_SMALL_UNROLL 2
 #endif
 constexpr int kSmallUnroll = B2_SMALL_UNROLL;  // j-loop unroll of the force task
-constexpr int kSmallImax = 32;   // own particles per CTA (at most; even)
+#ifndef B2_SMALL_IMAX
+#define B2_SMALL_IMAX 64
+#endif
+constexpr int kSmallImax = B2_SMALL_IMAX;  // own particles per CTA (at most; even)
 constexpr int kSmallMaxNP = 8;   // packed pairs per thread
 
 struct SmallArgs {
@@ -255,8 +258,8 @@ __global__ void __launch_bounds__(kSmallMaxThreads, 1) k_leapfrog_small(const Sm
     }
     ownv[t] = v;
   };
-  // warp 0 after its lanes t < I published: one arrival on counter blockIdx % 8 (release: the
-  // words are visible to whoever acquires the count)
+  // after the CTA's particles t < I were published: one arrival on the CTA's counter (release:
+  // the words are visible to whoever acquires the count)
 #ifndef B2_SMALL_WARPSYNC
 #define B2_SMALL_WARPSYNC 1
 #endif
@@ -266,8 +269,13 @@ __global__ void __launch_bounds__(kSmallMaxThreads, 1) k_leapfrog_small(const Sm
     const int C = gridDim.x;
     return B2_SMALL_WARPSYNC ? ((k + 1) * C + 7) / 8 - (k * C + 7) / 8 : (C - k + 7) / 8;
   };
+  // (after threads t < I stored their positions; called by the warps holding them: I <= 64)
+  const int pubw = (I + 31) >> 5;  // warps that publish
   auto announce = [&]() {
-    __syncwarp();
+    if (pubw > 1)
+      asm volatile("bar.sync 2, %0;" ::"r"(32 * pubw) : "memory");
+    else
+      __syncwarp();
     if (tid == 0) red_release_add_u32(a.arrive + 32 * counter_of(blockIdx.x), 1u);
   };
   // this warp: wait until the CTAs on the counters of its slice's producers published `state`
@@ -330,7 +338,7 @@ __global__ void __launch_bounds__(kSmallMaxThreads, 1) k_leapfrog_small(const Sm
     // opening kick + drift of step 0, publish state 1 (owna: written above by the same warps,
     // ordered by the named barrier; or loaded before the first barrier)
     if (tid < I) update(tid, false, 1);
-    if (tid < 32) announce();
+    if (tid < 32 * pubw) announce();
     for (int st = 0; st < a.nsteps; ++st) {
       B2_STRACE(0);
       __syncthreads();  // own[] holds this state; every read of part[] (reduce) is done
@@ -362,7 +370,7 @@ __global__ void __launch_bounds__(kSmallMaxThreads, 1) k_leapfrog_small(const Sm
       reduce_all();
       B2_STRACE(3);
       if (tid < I) update(tid, true, st + 1 < a.nsteps ? st + 2 : 0);
-      if (tid < 32 && st + 1 < a.nsteps) announce();
+      if (tid < 32 * pubw && st + 1 < a.nsteps) announce();
       B2_STRACE(4);
     }
   }
@@ -402,15 +410,16 @@ static bool small_shape(int n, int nch, int sms, SmallShape* s) {
   s->I = 2 * ((n + 2 * sms - 1) / (2 * sms));
   if (s->I > kSmallImax) return false;
   const int H = s->I / 2;
-  s->G = (H + kSmallMaxNP - 1) / kSmallMaxNP;
+  // pair groups: 1, 2 or 4 (a warp's lanes must map to whole chunks: G divides 32)
+  s->G = H <= kSmallMaxNP ? 1 : H <= 2 * kSmallMaxNP ? 2 : 4;
   s->NP = (H + s->G - 1) / s->G;
-  s->threads = std::max((s->G * nch + 31) / 32 * 32, 32);
+  s->threads = (std::max(s->G * nch, 4 * s->I) + 31) / 32 * 32;  // force tasks; the 4 I reduce rows
   s->ctas = (n + s->I - 1) / s->I;
   return s->threads <= kSmallMaxThreads && s->ctas <= sms && 32 % s->G == 0;
 }
 
 // The persistent small-N path of b2_leapfrog (k_leapfrog_small), when it applies:
-// fast arithmetic, n <= 32 x SMs, >= 2 j-chunks, tasks within one CTA, shared memory
+// fast arithmetic, n <= 64 x SMs, >= 2 j-chunks, tasks within one CTA, shared memory
 // fits, and the workspace holds small_workspace_bytes(n). Returns false
 // (nothing launched) otherwise.
 bool launch_leapfrog_small(int n, float4* pos, float4* vel, float4* acc, float eps, float dt, int nsteps,

@@ -96,13 +96,13 @@ class Leapfrog:
 
     One step: ``v += a h; x += v dt; a = calc_acc(x); v += a h`` with
     ``h = dt/2``. Steady state is two launches per step (force, fused update).
-    Up to 4736 particles the whole run is one persistent launch; between that and
+    Up to 64 x SMs particles (9472 on a B200) the whole run is one persistent launch; between that and
     ``GRAPH_MAX_N`` particles the per-step launches are the overhead, so ``step(k)``
     (k >= 2) is captured once per k into a CUDA graph and replayed (``graphs=False``
     turns that off; the same kernels run either way, so the results are identical).
     """
 
-    GRAPH_MIN_N = 4737
+    GRAPH_MIN_N = 9473
     GRAPH_MAX_N = 1 << 15
 
     pos: torch.Tensor

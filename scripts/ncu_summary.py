@@ -30,10 +30,10 @@ KEEP = {
                              "lts__throughput.avg.pct_of_peak_sustained_elapsed"],
 }
 NOTES = {
-    "k_force_fast": "N=2^20, 64 j-chunks: DRAM traffic is the 1 GiB partial-sum write; FP32-pipe (register-file) bound",
+    "k_force_fast": "N=2^20, 64 j-chunks reduced in-kernel in order (L2 ring, lines discarded): DRAM traffic ~ the 16 MiB in + 16 MiB out; FP32-pipe (register-file) bound",
     "k_diffusion_march": "512^3 step under ncu replay (cold L2); algorithmic 1.074 GB (8 B/cell)",
     "k_diffusion_tb2": "512^3, one launch = two steps, under ncu replay; algorithmic 1.074 GB (8 B/cell per launch)",
-    "k_leapfrog_small": "BASELINE configs[0]: N=4096, all 16 KDK steps in one persistent launch (147 CTAs); FP32 pipe ~half busy -- gather and step-to-step exchange latency",
+    "k_leapfrog_small": "BASELINE configs[0]: N=4096, all 16 KDK steps in one persistent launch (147 CTAs x 8 warps x 7 packed pairs, 128 j-chunks); the step-to-step exchange (arrival counters, bulk-copied slices, in-order reduce) is ~30% of a step",
     "k_diffusion_resident": "BASELINE configs[1]: 128^3 x 100 steps in one persistent launch (shared-memory-resident bricks); latency-bound per-step face exchange",
 }
 

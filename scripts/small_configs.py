@@ -26,7 +26,7 @@ def main():
         for r in range(args.reps):
             lf = b2.Leapfrog(torch.from_numpy(pos).to(dev), torch.from_numpy(vel).to(dev), 2.0 ** -6, 2.0 ** -7)
             torch.cuda.synchronize()
-            torch.cuda._sleep(100_000)  # host launch latency out of the events
+            torch.cuda._sleep(1_000_000)  # host launch latency out of the events
             ev[0].record()
             lf.step(16)
             ev[1].record()

@@ -76,7 +76,7 @@ def test_host_planning_entry_points(lib):
     # chunking depends on Nj only (sharding invariance); the in-kernel reduction's ring is
     # bounded (32 tiles of 2048 i x nch chunks: 64 MiB at 64 chunks), not nch x Ni x 16 B
     big = L.b2_calc_acc_workspace_bytes(1 << 20, 1 << 20, 0)
-    assert big == L.b2_calc_acc_workspace_bytes(1 << 22, 1 << 20, 0) <= (32 * 2048 * n20 * 16) + 512
+    assert big == L.b2_calc_acc_workspace_bytes(1 << 22, 1 << 20, 0) <= (32 * 2048 * n20 * 16) + 8192 + 128
     assert L.b2_calc_acc_workspace_bytes(1 << 19, 1 << 22, 0) < 65 << 20  # configs[3] shard: was 2 GiB
     assert L.b2_calc_acc_workspace_bytes(4096, 4096, 0) < big
     assert L.b2_calc_acc_workspace_bytes(100, 100, _lib.B2_EXACT) == 0

@@ -573,7 +573,8 @@ def test_leapfrog_persistent_small_n_bit_identical(tmp_path):
         "import paper_2411_18889_b200 as b2\n"
         "out = {}\n"
         "for n, steps, pot in [(4096, 16, False), (4096, 3, True), (3000, 5, False), (100, 4, True),\n"
-        "                      (4736, 2, False), (130, 0, False), (2048, 1, False)]:\n"
+        "                      (4736, 2, False), (130, 0, False), (2048, 1, False), (8192, 3, False),\n"
+        "                      (8192, 2, True), (9000, 2, False), (6144, 2, False)]:\n"
         "    pos, vel = b2.plummer_numpy(n, 7)\n"
         "    lf = b2.Leapfrog(torch.from_numpy(pos).cuda(), torch.from_numpy(vel).cuda(), 2.0 ** -6, 2.0 ** -7,\n"
         "                     potential=pot)\n"
@@ -594,11 +595,11 @@ def test_leapfrog_persistent_small_n_bit_identical(tmp_path):
         assert bits_equal(res["1"][k], res["0"][k]), k
 
 
-@pytest.mark.parametrize("n", [4096, 8192])
+@pytest.mark.parametrize("n", [4096, 8192, 12288])
 def test_leapfrog_time_reversible(b2, n):
     """Leapfrog is time-symmetric: k steps forward, velocities negated, k steps back return
-    the initial positions to FP32 round-off (persistent one-launch path at 4096, graph-replayed
-    two-kernel path at 8192)."""
+    the initial positions to FP32 round-off (persistent one-launch path at 4096 and 8192,
+    graph-replayed two-kernel path at 12288)."""
     pos, vel = b2.plummer(n, 11)
     fw = b2.Leapfrog(pos.clone(), vel.clone(), 2.0 ** -6, 2.0 ** -7)
     fw.step(64)
@@ -612,7 +613,7 @@ def test_leapfrog_time_reversible(b2, n):
 def test_leapfrog_graph_replay_bit_identical(b2):
     """Mid-N Leapfrog.step(k) replays a captured CUDA graph of b2_leapfrog(k); same kernels,
     same bits as direct launches, across repeated and mixed step counts."""
-    pos, vel = b2.plummer(8192, 5)
+    pos, vel = b2.plummer(12288, 5)
     a = b2.Leapfrog(pos.clone(), vel.clone(), 2.0 ** -6, 2.0 ** -7)
     b = b2.Leapfrog(pos.clone(), vel.clone(), 2.0 ** -6, 2.0 ** -7, graphs=False)
     for k in (4, 4, 3, 1, 4):

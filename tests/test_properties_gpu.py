@@ -83,7 +83,7 @@ def test_calc_acc_any_sizes(b2, restatement, ni, nj, potential, seed):
 
 @settings(max_examples=30, deadline=None, derandomize=True,
           suppress_health_check=[HealthCheck.function_scoped_fixture, HealthCheck.too_slow])
-@given(n=st.integers(2, 4736), steps=st.integers(0, 4), potential=st.booleans(), seed=st.integers(0, 2 ** 16))
+@given(n=st.integers(2, 9472), steps=st.integers(0, 4), potential=st.booleans(), seed=st.integers(0, 2 ** 16))
 def test_leapfrog_small_n_tracks_oracle(b2, restatement, n, steps, potential, seed):
     """The persistent small-N leapfrog (and the two-kernel path it must equal) against the oracle KDK."""
     pos, vel = b2.plummer_numpy(n, seed)
