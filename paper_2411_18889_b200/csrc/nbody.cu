@@ -458,7 +458,7 @@ static const ForceVariant kVariants[] = {
     B2_FV(128, 16, 2, 2, 3, 2),  // 8
     B2_FV(256, 8, 2, 4, 3, 1),   // 9: 1 of 4
     B2_FV(64, 2, 16, 4, 2, 0),   // 10: small N
-    B2_FV(32, 8, 16, 4, 2, 0),   // 11: 32-j chunks (Nj <= kFineChunkNj, e.g. configs[0]: N=4096)
+    B2_FV(32, 8, 16, 4, 2, 0),   // 11: chunks of an odd multiple of 32 j (Nj <= kAlign32Nj, e.g. N=4096)
 };
 #undef B2_FV
 
@@ -479,7 +479,7 @@ static int large_variant() {
 // The variant launch_partials / launch_fused take for Ni (same per-lane arithmetic and j
 // order in every variant, so the choice never moves a bit).
 static const ForceVariant* pick_variant(int Ni, int nch, int jchunk) {
-  if (jchunk < 64) return &kVariants[11];  // a j tile never spans two chunks' worth of padding
+  if (jchunk % 64) return &kVariants[11];  // 32-j tiles: no padding in 32-aligned chunks
   const ForceVariant* v = &kVariants[large_variant()];
   static const long long want_k = std::max(0, env_int_nb("SOLOMON_NBODY_WANT", 4));  // tuning knob: CTAs per SM
   const long long want = want_k * device_info().sms;

@@ -83,14 +83,15 @@ __device__ __forceinline__ void interact_bf(const float2 X, const float2 Y, cons
 // order). Large Nj: ~64 chunks, 64-aligned (the tile kernel's waves and ring). Nj up to
 // kFineChunkNj: ~128 chunks, 32-aligned -- the persistent small-N leapfrog's parallelism
 // is (own particles / 2) x chunks per SM, and 128 chunks give it 8 warps x 7 packed pairs
-// at N = 4096 (64 chunks left it at 14 warps x 2 pairs, ~55% of the FMA pipe). Above that
-// (its 4-group shape, n <= 64 x SMs) 64 chunks already fill its 256 threads.
-constexpr int kFineChunkNj = 4736;
+// at N = 4096 (64 chunks left it at 14 warps x 2 pairs, ~55% of the FMA pipe). Up to
+// kAlign32Nj: ~64 chunks, 32-aligned, so that its 4 pair groups x chunks fill 8 warps
+// evenly (9472: 60 chunks of 160 instead of 50 of 192, which left 7 warps on 4 schedulers).
+constexpr int kFineChunkNj = 4736, kAlign32Nj = 9472;
 constexpr int kFineChunks = 128, kFineAlign = 32;
 inline int chunk_size(int Nj, int flags) {
   if (flags & B2_EXACT) return Nj;
   const int target = Nj <= kFineChunkNj ? kFineChunks : kTargetChunks;
-  const int align = Nj <= kFineChunkNj ? kFineAlign : kChunkAlign;
+  const int align = Nj <= kAlign32Nj ? kFineAlign : kChunkAlign;
   int c = (Nj + target - 1) / target;
   c = (c + align - 1) / align * align;
   return std::max(c, align);
