@@ -12,6 +12,11 @@ for pot in (False, True):
 big, _ = b2.plummer(40000, 2)
 b2.accelerations(big[:20000].contiguous(), 2 ** -6, big)     # large variant path
 lf = b2.Leapfrog(pos.clone(), vel.clone(), 2 ** -6, 2 ** -7); lf.step(3)
+huge, _ = b2.plummer(70000, 3)
+b2.accelerations(huge, 2 ** -6, huge[:4096].contiguous())   # Ni > 63488: in-kernel ring reduction
+for n in (4096, 8192):                                      # persistent path: 2 and 4 pair groups
+    p2, v2 = b2.plummer(n, 4)
+    b2.Leapfrog(p2, v2, 2 ** -6, 2 ** -7, potential=n == 8192).step(2)
 for shape in [(20, 24, 128), (7, 5, 9), (5, 3, 512), (3, 4, 100)]:
     f = torch.rand(shape, device=dev); fn = torch.empty_like(f)
     b2.diffusion3d(*shape, 0.1, 0.1, 0.1, 1e-3, 1.0, f, fn)
