@@ -1,4 +1,2 @@
 mkdir -p gpurun_out
-timeout 600 python scripts/leapfrog_sizes.py 4096 4736 5120 6144 7168 8192 9472 12288 > gpurun_out/lf_sizes.log 2>&1
-timeout 900 python -m pytest tests -m gpu -x -q -p no:cacheprovider > gpurun_out/gputest_small.log 2>&1
-echo rc=$? >> gpurun_out/gputest_small.log
+for m in 64 128; do for w in 4 2; do echo "== midchunks $m want $w"; SOLOMON_NBODY_WANT=$w SOLOMON_NBODY_MIDCHUNKS=$m timeout 600 python scripts/leapfrog_sizes.py 12288 16384 24576 32768; done; done > gpurun_out/lf_mid.log 2>&1
