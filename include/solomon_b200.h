@@ -129,7 +129,10 @@ const char *b2_fault_kernel(int which);
  * unsharded one. 1 for B2_EXACT. */
 int b2_calc_acc_nchunks(int Nj, int flags);
 
-/* Scratch bytes b2_calc_acc needs (0 when nchunks == 1). */
+/* Scratch bytes b2_calc_acc needs (0 when nchunks == 1): all nchunks x Ni
+ * partials up to ~63k i (summed by a second launch), beyond that a ring of 32
+ * i-tiles the force kernel sums in place -- at most ~64 MiB at 64 chunks
+ * (N = 2^20 and 2^22 alike). Same bits either way. */
 size_t b2_calc_acc_workspace_bytes(int Ni, int Nj, int flags);
 
 /* iacc[i] = sum_j m_j (r_j - r_i) / (|r_j - r_i|^2 + eps^2)^{3/2}, i < Ni. */
@@ -161,7 +164,7 @@ int b2_kdk_update_publish(int n, const float *pos_in, float *pos_out, float *vel
 
 /* Whole single-device leapfrog: nsteps KDK steps of the self-gravitating
  * system pos[n] (acc must hold a(pos) on entry unless B2_INIT_ACC is set;
- * holds a(pos) on exit). Small systems (n <= 32 x SMs, fast arithmetic) run
+ * holds a(pos) on exit). Small systems (n <= 64 x SMs, fast arithmetic) run
  * every step in one persistent launch; otherwise two launches per step. Both
  * give the same bits. */
 #define B2_INIT_ACC 4
