@@ -55,6 +55,8 @@ typedef struct solomon_float4 {
                            cudaError_t of the failed cudaMalloc)             */
 #define B2_ETIMEOUT (-5) /* a device-side wait for data another CTA or GPU
                             publishes gave up (b2_fault_status)              */
+#define B2_ENOTSUP (-6) /* no kernel for this shape on this path (e.g. no
+                            two-steps-per-pass plan: b2_diffusion3d_run2_planes) */
 /* positive values are cudaError_t codes from the launch / copy / allocation */
 
 /* ---- b2_calc_acc flags --------------------------------------------------- */
@@ -245,6 +247,16 @@ int b2_diffusion3d_slab_halo2(int nx_ext, int ny, int nz, int lo_h, int nx_local
  * is in fn, 0 when it is in f; the other buffer is scratch. */
 int b2_diffusion3d_run(int nx, int ny, int nz, float dx, float dy, float dz, float dt, float kappa,
                        float *f, float *fn, int nsteps, int *result_in_fn, void *stream);
+
+/* Two steps f -> fn written ONLY to fn's planes [p0, p1) and [p2, p3) (disjoint;
+ * either may be empty; the rest of fn is untouched), reading f's planes within two
+ * of them, clamped at 0 / nx-1 -- the same bits as those planes of
+ * b2_diffusion3d_run(..., 2, ...). For slabs that overlap a halo exchange with the
+ * pass: the planes that need no halo first, then the two next to each halo (one
+ * launch for both) once it arrived. Uses the two-steps-per-pass kernel; B2_ENOTSUP
+ * when the shape has no plan for it (empty ranges only ask). */
+int b2_diffusion3d_run2_planes(int nx, int ny, int nz, float dx, float dy, float dz, float dt, float kappa,
+                               const float *f, float *fn, int p0, int p1, int p2, int p3, void *stream);
 
 /* --- Peer memory across processes (multi-GPU fused halo) --- */
 

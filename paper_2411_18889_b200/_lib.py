@@ -21,6 +21,7 @@ B2_EALIGN = -2
 B2_ESPACE = -3
 B2_ENOMEM = -4
 B2_ETIMEOUT = -5
+B2_ENOTSUP = -6
 B2_POTENTIAL = 1
 B2_EXACT = 2
 B2_INIT_ACC = 4
@@ -56,6 +57,7 @@ SIGNATURES = {
     "b2_diffusion3d_plan": (_i, [_i, _i, _i, _f, _f, _f, _f, _f, _p, _p, _i, _p]),
     "b2_diffusion3d_slab": (_i, [_i, _i, _i, _f, _f, _f, _f, _f, _p, _p, _p, _p, _i, _i, _p]),
     "b2_diffusion3d_run": (_i, [_i, _i, _i, _f, _f, _f, _f, _f, _p, _p, _i, ctypes.POINTER(_i), _p]),
+    "b2_diffusion3d_run2_planes": (_i, [_i, _i, _i, _f, _f, _f, _f, _f, _p, _p, _i, _i, _i, _i, _p]),
     "b2_diffusion3d_mailbox_bytes": (_sz, [_i, _i]),
     "b2_diffusion3d_slab_edges": (_i, [_i, _i, _i, _f, _f, _f, _f, _f, _p, _p, _p, _p, _p, _p, _i, _i, _p]),
     "b2_diffusion3d_mailbox2_bytes": (_sz, [_i, _i]),

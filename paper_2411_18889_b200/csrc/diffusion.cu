@@ -569,5 +569,17 @@ int b2_diffusion3d_run(int nx, int ny, int nz, float dx, float dy, float dz, flo
   return B2_OK;
 }
 
+int b2_diffusion3d_run2_planes(int nx, int ny, int nz, float dx, float dy, float dz, float dt, float kappa,
+                               const float* f, float* fn, int p0, int p1, int p2, int p3, void* stream) {
+  if (int rc = check_grid(nx, ny, nz, f, fn)) return rc;
+  if (p0 < 0 || p1 > nx || p0 > p1 || p2 < 0 || p3 > nx || p2 > p3 || (p2 < p3 && p0 < p1 && p2 < p1 && p0 < p3))
+    return B2_EINVAL;
+  TB2Plan tb;
+  if (nz % 4 != 0 || !aligned16(f) || !aligned16(fn) || !plan_tb2_lookup(nx, ny, nz, tb)) return B2_ENOTSUP;
+  if (p0 == p1 && p2 == p3) return B2_OK;
+  if (p0 == p1) std::swap(p0, p2), std::swap(p1, p3);
+  return launch_tb2(tb, nx, ny, nz, make_coefs(dx, dy, dz, dt, kappa), f, fn, as_stream(stream), p0, p1, p2, p3);
+}
+
 }  // extern "C"
 

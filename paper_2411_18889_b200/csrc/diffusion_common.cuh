@@ -117,7 +117,10 @@ struct TB2Plan {
 bool plan_tb2(int nx, int ny, int nz, TB2Plan& best);
 bool plan_tb2_lookup(int nx, int ny, int nz, TB2Plan& best);  // tuned plan if planned, else the model's pick
 int plan_tb2_tune(int nx, int ny, int nz, const Coefs& c, const float* f, float* fn, cudaStream_t s);
-int launch_tb2(const TB2Plan& p, int nx, int ny, int nz, const Coefs& c, const float* f, float* fn, cudaStream_t s);
+// two steps; output planes [i_lo, i_hi) (default: all) and [i_lo2, i_hi2) of fn only,
+// inputs clamped at 0 / nx-1
+int launch_tb2(const TB2Plan& p, int nx, int ny, int nz, const Coefs& c, const float* f, float* fn, cudaStream_t s,
+               int i_lo = 0, int i_hi = -1, int i_lo2 = 0, int i_hi2 = 0);
 
 // ---- shared-memory-resident time loop (diffusion_resident.cu) ----
 // Launches all nsteps for grids that fit the SMs' shared memory; false if not applicable

@@ -47,6 +47,8 @@ struct TB2Args {
   int nx, ny, nz;
   int TJ, n_jtiles, IC, nst, ns1;
   int R, R1;  // rows per input-ring slot / per step-1 slot
+  int i_lo, i_hi;  // output planes [i_lo, i_hi): the whole grid, or a slab's interior / edges
+  int i_lo2, i_hi2, splits1;  // i-splits >= splits1 cover a second range (a slab's two edges, one launch)
   Coefs c;
 };
 
@@ -79,7 +81,9 @@ __global__ void __launch_bounds__(kTBThreads, 1) k_diffusion_tb2(const TB2Args a
 
   const int jt = blockIdx.x % a.n_jtiles, ic = blockIdx.x / a.n_jtiles;
   const int j0 = jt * TJ, rows = min(TJ, ny - j0);
-  const int i0 = ic * a.IC, i1 = min(i0 + a.IC, nx);
+  const bool second = ic >= a.splits1;
+  const int i0 = second ? a.i_lo2 + (ic - a.splits1) * a.IC : a.i_lo + ic * a.IC;
+  const int i1 = min(i0 + a.IC, second ? a.i_hi2 : a.i_hi);
   if (i0 >= i1) return;                                               // uniform per CTA
   const int qlo = max(i0 - 1, 0), qhi = min(i1, nx - 1);              // step-1 planes
   const int lo_in = max(qlo - 1, 0), hi_in = min(qhi + 1, nx - 1);    // input planes
@@ -410,10 +414,22 @@ static void launch_tb2_t(const TB2Plan& p, const TB2Args& a, cudaStream_t s) {
 }
 
 int launch_tb2(const TB2Plan& p, int nx, int ny, int nz, const Coefs& c, const float* f, float* fn,
-                      cudaStream_t s) {
-  TB2Args a{f, fn, nx, ny, nz, p.TJ, p.n_jtiles, p.IC, p.nst, p.ns1, p.R, p.R1, c};
+                      cudaStream_t s, int i_lo, int i_hi, int i_lo2, int i_hi2) {
+  if (i_hi < 0) i_hi = nx;
+  TB2Plan q = p;
+  int splits1 = (nx + p.IC - 1) / p.IC;
+  if (i_lo != 0 || i_hi != nx || i_hi2 > i_lo2) {  // plane ranges: the plan's i-split length, re-spread
+    const int len = i_hi - i_lo, len2 = std::max(i_hi2 - i_lo2, 0);
+    const int longest = std::max(len, len2);
+    if (longest <= 0) return B2_OK;
+    const int splits = (longest + p.IC - 1) / p.IC;
+    q.IC = (longest + splits - 1) / splits;
+    splits1 = len > 0 ? (len + q.IC - 1) / q.IC : 0;
+    q.grid = q.n_jtiles * (splits1 + (len2 + q.IC - 1) / q.IC);
+  }
+  TB2Args a{f, fn, nx, ny, nz, q.TJ, q.n_jtiles, q.IC, q.nst, q.ns1, q.R, q.R1, i_lo, i_hi, i_lo2, i_hi2, splits1, c};
 #define B2_TB2_CASE(A, B) \
-  if (p.S1 == A && p.S2 == B) launch_tb2_t<A, B>(p, a, s); else
+  if (q.S1 == A && q.S2 == B) launch_tb2_t<A, B>(q, a, s); else
   B2_TB2_CASE(2, 1) B2_TB2_CASE(2, 2) B2_TB2_CASE(3, 2) B2_TB2_CASE(3, 3) B2_TB2_CASE(4, 3) B2_TB2_CASE(4, 4)
   B2_TB2_CASE(5, 3) B2_TB2_CASE(5, 4) B2_TB2_CASE(6, 4) B2_TB2_CASE(6, 5) B2_TB2_CASE(6, 6) return B2_EINVAL;
 #undef B2_TB2_CASE

@@ -128,6 +128,7 @@ const char* b2_error_string(int code) {
     case B2_ESPACE: return "workspace too small";
     case B2_ENOMEM: return "out of device memory";
     case B2_ETIMEOUT: return "a device-side wait for a peer's data timed out (see b2_fault_status)";
+    case B2_ENOTSUP: return "no kernel for this shape on this path";
     default: return code > 0 ? cudaGetErrorString(static_cast<cudaError_t>(code)) : "unknown error";
   }
 }

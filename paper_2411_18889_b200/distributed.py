@@ -98,6 +98,17 @@ class CudaSlabKernels:
                                                ctypes.byref(in_fn), _lib.stream_handle(f.device)), "diffusion3d_run")
         return bool(in_fn.value)
 
+    def run2_planes(self, f, fn, p0: int, p1: int, p2: int = 0, p3: int = 0) -> bool:
+        """Two steps over a (halo-extended) slab written only to fn[p0:p1] and fn[p2:p3]
+        (b2_diffusion3d_run2_planes); False when the shape has no kernel for it."""
+        nx, ny, nz = f.shape
+        rc = self.lib.b2_diffusion3d_run2_planes(nx, ny, nz, *self.args, f.data_ptr(), fn.data_ptr(), p0, p1, p2, p3,
+                                                  _lib.stream_handle(f.device))
+        if rc == _lib.B2_ENOTSUP:
+            return False
+        _lib.check(rc, "diffusion3d_run2_planes")
+        return True
+
 
 def _all_gather_inplace(out: torch.Tensor, local: torch.Tensor, group=None) -> None:
     if dist.get_backend(group) == "nccl":
@@ -621,7 +632,15 @@ class SlabDiffusion:
         if pairs:
             nxl, lo_h = self.f.shape[0], self._lo_h
             cur, oth = self._ext if self.f.data_ptr() == self._ext[0][lo_h].data_ptr() else self._ext[::-1]
+            # overlap: the planes that need no halo computed while it travels (world > 1, slabs
+            # of >= 6 planes, a kernel that writes a plane range); else refresh, then the pass
+            overlap = (self.world > 1 and nxl >= 6 and hasattr(self.k, "run2_planes")
+                       and self.k.run2_planes(cur, oth, 0, 0))
             for _ in range(pairs):
+                if overlap:
+                    self._pass_overlapped(cur, oth, lo_h, nxl)
+                    cur, oth = oth, cur
+                    continue
                 self._halo2(cur, lo_h, nxl)
                 if self.k.run2(cur, oth):
                     cur, oth = oth, cur
@@ -632,6 +651,48 @@ class SlabDiffusion:
         if nsteps % 2:
             self.step(1)
         return self.f
+
+    def _pass_overlapped(self, cur: torch.Tensor, oth: torch.Tensor, lo_h: int, nxl: int) -> None:
+        """One two-step pass cur -> oth with the halo exchange overlapped: the neighbours' two
+        edge planes travel (NCCL on the comm stream, or the p2p push on the side stream) while
+        the planes that need no halo -- all but the two next to each neighbour -- are computed;
+        then the two planes next to each halo. Output plane p reads input planes p-2 .. p+2 only,
+        so every plane gets the bits of the whole-slab pass."""
+        lo_e = lo_h + (2 if self.has_lo else 0)          # first plane that needs no low halo
+        hi_e = lo_h + nxl - (2 if self.has_hi else 0)    # one past the last that needs no high halo
+        if self.transport == "p2p":
+            if self._closed:
+                raise RuntimeError("SlabDiffusion: the p2p transport was closed")
+            nx_ext, ny, nz = cur.shape
+            xchg = getattr(self, "_xchg", 0)
+            lib, main = _lib.load(), torch.cuda.current_stream(cur.device)
+            halo2 = lambda phase, stream: _lib.check(lib.b2_diffusion3d_slab_halo2(  # noqa: E731
+                nx_ext, ny, nz, lo_h, nxl, cur.data_ptr(), *self._in2, *self._out2, xchg, phase,
+                stream.cuda_stream), "diffusion3d_slab_halo2")
+            self._side.wait_stream(main)   # cur's edge planes are final
+            halo2(0, self._side)           # push them to the neighbours, beside the interior
+            self.k.run2_planes(cur, oth, lo_e, hi_e)
+            halo2(1, main)                 # the neighbours' planes into cur's halo
+            self._xchg = xchg + 1
+            main.wait_stream(self._side)   # the push read cur: done before a pass overwrites it
+        else:
+            ops, g = [], self.group
+            if self.has_lo:
+                ops.append(dist.P2POp(dist.isend, cur[lo_h:lo_h + 2], self.rank - 1, g))
+                ops.append(dist.P2POp(dist.irecv, cur[0:2], self.rank - 1, g))
+            if self.has_hi:
+                ops.append(dist.P2POp(dist.isend, cur[lo_h + nxl - 2:lo_h + nxl], self.rank + 1, g))
+                ops.append(dist.P2POp(dist.irecv, cur[lo_h + nxl:lo_h + nxl + 2], self.rank + 1, g))
+            if self.is_cuda:
+                self.comm.wait_stream(torch.cuda.current_stream(cur.device))
+                with torch.cuda.stream(self.comm):
+                    reqs = dist.batch_isend_irecv(ops)
+            else:
+                reqs = dist.batch_isend_irecv(ops)
+            self.k.run2_planes(cur, oth, lo_e, hi_e)
+            for r in reqs:
+                r.wait()  # NCCL: the current stream waits for the exchange; gloo: the host does
+        self.k.run2_planes(cur, oth, lo_h, lo_e, hi_e, lo_h + nxl)  # both edges, one launch
 
     def _halo2(self, cur: torch.Tensor, lo_h: int, nxl: int) -> None:
         """Fill cur's halo planes with the neighbours' two edge planes of the same state."""

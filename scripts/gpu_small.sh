@@ -1,2 +1,4 @@
 mkdir -p gpurun_out
-for m in 64 128; do for w in 4 2; do echo "== midchunks $m want $w"; SOLOMON_NBODY_WANT=$w SOLOMON_NBODY_MIDCHUNKS=$m timeout 600 python scripts/leapfrog_sizes.py 12288 16384 24576 32768; done; done > gpurun_out/lf_mid.log 2>&1
+(python scripts/slab_split_cost.py 1024; python scripts/slab_split_cost.py 512) > gpurun_out/slab_split.log 2>&1
+timeout 1200 python -m pytest tests -m gpu -x -q -p no:cacheprovider -k "run2_planes or p2p or distributed or slab or temporal or bit_identical" > gpurun_out/gputest_slab.log 2>&1
+echo rc=$? >> gpurun_out/gputest_slab.log

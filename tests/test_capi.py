@@ -93,6 +93,11 @@ def test_argument_validation_before_any_device_work(lib):
     assert L.b2_calc_acc(4, 16, 32, 4, 16, 0.1, 64, None, 0, None) == _lib.B2_EINVAL  # unknown flag
     assert L.b2_diffusion3d(0, 4, 4, 1.0, 1.0, 1.0, 0.1, 1.0, 16, 32, None) == _lib.B2_EINVAL
     assert L.b2_diffusion3d(4, 4, 4, 1.0, 1.0, 1.0, 0.1, 1.0, 16, 16, None) == _lib.B2_EINVAL  # f == fn
+    r2p = lambda *r: L.b2_diffusion3d_run2_planes(4, 4, 4, 1.0, 1.0, 1.0, 0.1, 1.0, 16, 32, *r, None)  # noqa: E731
+    assert r2p(3, 2, 0, 0) == _lib.B2_EINVAL  # p0 > p1
+    assert r2p(0, 5, 0, 0) == _lib.B2_EINVAL  # past nx
+    assert r2p(0, 3, 2, 4) == _lib.B2_EINVAL  # overlapping ranges
+    assert L.b2_error_string(_lib.B2_ENOTSUP) == b"no kernel for this shape on this path"
     assert L.b2_diffusion3d_slab(4, 4, 4, 1.0, 1.0, 1.0, 0.1, 1.0, 16, None, None, 32, 3, 2, None) == _lib.B2_EINVAL
     assert L.b2_kdk_update(4, None, None, 16, None, 1, 0.0, 0.0, 0.0, 8, None) == _lib.B2_EINVAL
     # fused slab halo: mailbox sizing and validation (no device work)

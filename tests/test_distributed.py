@@ -50,6 +50,13 @@ class OracleSlabKernels:
         fn.numpy()[...] = self.o.diffusion_run(f.numpy(), 2, *self.args)
         return True
 
+    def run2_planes(self, f, fn, p0, p1, p2=0, p3=0):
+        if p1 > p0 or p3 > p2:
+            out = self.o.diffusion_run(f.numpy(), 2, *self.args)
+            fn.numpy()[p0:p1] = out[p0:p1]
+            fn.numpy()[p2:p3] = out[p2:p3]
+        return True
+
     def slab(self, f, fn, halo_lo, halo_hi, i_begin, i_end):
         a = f.numpy()
         lo = halo_lo.numpy() if halo_lo is not None else a[0]  # absent halo == clamp IMAX(i-1,0)
@@ -366,10 +373,12 @@ def _run2_worker(rank, world, port, counts, ny, nz, steps, out_path):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,counts,steps", [(2, (3, 4), (4, 5)), (3, (2, 5, 3), (6, 2)), (4, (2, 2, 3, 2), (3, 4))])
+@pytest.mark.parametrize("world,counts,steps", [(2, (3, 4), (4, 5)), (3, (2, 5, 3), (6, 2)), (4, (2, 2, 3, 2), (3, 4)),
+                                               (2, (7, 9), (4, 5)), (3, (6, 8, 11), (6, 3))])
 def test_slab_run_two_steps_per_exchange_equals_full_grid(tmp_path, world, counts, steps):
     """SlabDiffusion.run: two steps per exchange of two halo planes (uneven slabs, odd
-    remainders, mixed with step()) == the full-grid oracle run, bit for bit."""
+    remainders, mixed with step(); slabs of >= 6 planes take the overlapped pass -- interior
+    while the halo travels, then the planes next to it) == the full-grid oracle run, bit for bit."""
     import oracle
 
     out = tmp_path / "r.npy"

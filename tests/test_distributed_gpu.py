@@ -209,10 +209,12 @@ def _p2p_run_worker(rank, world, port, counts, ny, nz, steps, out, lag=0.0):
 
 
 @pytest.mark.parametrize("world,counts,ny,nz,steps", [(2, (3, 5), 20, 64, (4, 3)), (3, (2, 4, 3), 9, 1024, (6, 2)),
-                                                      (4, (9, 7, 8, 8), 40, 128, (5, 6))])
+                                                      (4, (9, 7, 8, 8), 40, 128, (5, 6)),
+                                                      (2, (12, 10), 24, 256, (6, 3)), (3, (6, 16, 7), 33, 512, (4, 5))])
 def test_p2p_run_two_steps_per_exchange(tmp_path, world, counts, ny, nz, steps):
     """SlabDiffusion.run over the p2p transport: two-plane halos through peer-memory mailboxes
-    (b2_diffusion3d_slab_halo2) every two steps, mixed with step(); bit-identical."""
+    (b2_diffusion3d_slab_halo2) every two steps, mixed with step(); slabs of >= 6 planes overlap
+    the push with the planes that need no halo (b2_diffusion3d_run2_planes); bit-identical."""
     import torch.multiprocessing as mp
 
     out = tmp_path / "run2.npz"
@@ -228,6 +230,10 @@ def test_p2p_run_waits_for_a_late_neighbour(tmp_path):
 
     out = tmp_path / "runlag.npz"
     mp.spawn(_p2p_run_worker, args=(2, _port(), (4, 5), 12, 64, (6, 2), str(out), 0.3), nprocs=2, join=True)
+    z = np.load(out)
+    assert np.array_equal(z["got"].view(np.uint32), z["want"].view(np.uint32))
+    out = tmp_path / "runlag2.npz"  # the overlapped pass (slabs of >= 6 planes)
+    mp.spawn(_p2p_run_worker, args=(2, _port(), (8, 9), 12, 128, (6, 2), str(out), 0.3), nprocs=2, join=True)
     z = np.load(out)
     assert np.array_equal(z["got"].view(np.uint32), z["want"].view(np.uint32))
 

@@ -651,3 +651,29 @@ def test_checkpoint_resume_single_device(b2, tmp_path):
     b2.load_checkpoint(g, tmp_path / "df.pt")
     g.run(4)
     assert bits_equal(d.field.cpu().numpy(), g.field.cpu().numpy()) and g.steps == 7
+
+
+@pytest.mark.parametrize("shape,ranges", [((40, 24, 128), [(2, 38), (0, 2, 38, 40)]),
+                                          ((19, 33, 512), [(5, 11), (0, 5), (11, 19)]),
+                                          ((23, 20, 256), [(2, 21), (0, 0, 21, 23), (0, 2)]),
+                                          ((12, 9, 1024), [(0, 12)])])
+def test_run2_planes_equals_the_whole_pass(b2, shape, ranges):
+    """b2_diffusion3d_run2_planes: two steps written only to one or two plane ranges -- pieced
+    together over any split of the planes, bit-identical to b2_diffusion3d_run(..., 2); planes
+    outside the ranges untouched."""
+    from paper_2411_18889_b200.distributed import CudaSlabKernels
+
+    args = (0.1, 0.12, 0.09, 1e-3, 1.0)
+    f = torch.rand(shape, device="cuda")
+    want = b2.Diffusion3D(f.clone(), *args).run(2).clone()
+    k = CudaSlabKernels(*args)
+    fn = torch.full_like(f, float("nan"))
+    for r in ranges[1:]:
+        assert k.run2_planes(f, fn, *r)
+    assert torch.isnan(fn[ranges[0][0]:ranges[0][1]]).all()  # untouched so far
+    assert k.run2_planes(f, fn, *ranges[0])
+    torch.cuda.synchronize()
+    assert bits_equal(fn.cpu().numpy(), want.cpu().numpy())
+    assert k.run2_planes(f, fn, 3, 3)  # empty range: just asks
+    odd = torch.rand((6, 8, 100), device="cuda")  # nz % 4 != 0: no two-steps-per-pass kernel
+    assert not k.run2_planes(odd, torch.empty_like(odd), 0, 6)
