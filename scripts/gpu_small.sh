@@ -1,4 +1,2 @@
 mkdir -p gpurun_out
-(python scripts/slab_split_cost.py 1024; python scripts/slab_split_cost.py 512) > gpurun_out/slab_split.log 2>&1
-timeout 1200 python -m pytest tests -m gpu -x -q -p no:cacheprovider -k "run2_planes or p2p or distributed or slab or temporal or bit_identical" > gpurun_out/gputest_slab.log 2>&1
-echo rc=$? >> gpurun_out/gputest_slab.log
+for b in trace_small trace_small_ldg trace_small trace_small_ldg; do echo "== $b"; ./scripts/$b 4096 40; ./scripts/$b 8192 40; done > gpurun_out/trace_small.log 2>&1
