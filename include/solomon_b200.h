@@ -119,6 +119,10 @@ long long b2_poll_timeout_ms(void);
  * per step. */
 int b2_fault_status(void *stream, int clear, int *which);
 const char *b2_fault_kernel(int which);
+/* Test hook: CTA `cta` of b2_leapfrog's persistent small-N path never announces
+ * its positions in later launches (-1: none), so the other CTAs' waits expire --
+ * exercises the watchdog path (tests/test_faults_gpu.py). */
+int b2_debug_withhold_publish(int cta);
 
 /* =========================================================================
  * 2. Stream-ordered API (device pointers; `stream` is a cudaStream_t or NULL)

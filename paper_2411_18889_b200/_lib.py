@@ -57,6 +57,7 @@ SIGNATURES = {
     "b2_diffusion3d_plan": (_i, [_i, _i, _i, _f, _f, _f, _f, _f, _p, _p, _i, _p]),
     "b2_diffusion3d_slab": (_i, [_i, _i, _i, _f, _f, _f, _f, _f, _p, _p, _p, _p, _i, _i, _p]),
     "b2_diffusion3d_run": (_i, [_i, _i, _i, _f, _f, _f, _f, _f, _p, _p, _i, ctypes.POINTER(_i), _p]),
+    "b2_debug_withhold_publish": (_i, [_i]),
     "b2_diffusion3d_run2_planes": (_i, [_i, _i, _i, _f, _f, _f, _f, _f, _p, _p, _i, _i, _i, _i, _p]),
     "b2_diffusion3d_mailbox_bytes": (_sz, [_i, _i]),
     "b2_diffusion3d_slab_edges": (_i, [_i, _i, _i, _f, _f, _f, _f, _f, _p, _p, _p, _p, _p, _p, _i, _i, _p]),

@@ -37,6 +37,9 @@ struct Watch {
   unsigned long long timeout_ns;
 };
 Watch make_watch();
+// test hook (b2_debug_withhold_publish): the CTA of the persistent small-N leapfrog that never
+// announces its positions, so the watchdog path can be exercised; -1 = none
+int debug_withhold();
 // fault codes (which kernel gave up), reported by b2_fault_status / b2_fault_kernel
 constexpr unsigned int kFaultLeapfrogSmall = 1, kFaultResident = 2, kFaultSlabEdges = 3, kFaultHalo2 = 4,
                        kFaultForceRing = 5;

@@ -67,6 +67,7 @@ struct SmallArgs {
   int I;  // own particles per CTA: 2 * ceil(n / (2 * SMs)) <= 32, so the grid spans every SM
   int G;  // pair groups per CTA (threads = G * nch, rounded up to a warp)
   Watch watch;  // a position word that never arrives ends the run (runtime.cu), no trap
+  int withhold;  // test hook: this CTA never announces (b2_debug_withhold_publish), -1 = none
 #ifdef B2_SMALL_TRACE
   unsigned long long* trace;  // [cta][step][32] globaltimer stamps (scripts/trace_small.cu)
 #endif
@@ -276,7 +277,8 @@ __global__ void __launch_bounds__(kSmallMaxThreads, 1) k_leapfrog_small(const Sm
       asm volatile("bar.sync 2, %0;" ::"r"(32 * pubw) : "memory");
     else
       __syncwarp();
-    if (tid == 0) red_release_add_u32(a.arrive + 32 * counter_of(blockIdx.x), 1u);
+    if (tid == 0 && static_cast<int>(blockIdx.x) != a.withhold)
+      red_release_add_u32(a.arrive + 32 * counter_of(blockIdx.x), 1u);
   };
   // this warp: wait until the CTAs on the counters of its slice's producers published `state`
   auto slice_published = [&](int state) -> bool {
@@ -464,7 +466,7 @@ bool launch_leapfrog_small(int n, float4* pos, float4* vel, float4* acc, float e
     return false;
   }
   SmallArgs args{n, pos, vel, acc, pub, reinterpret_cast<unsigned int*>(pub + 2 * static_cast<size_t>(n)), eps * eps, dt, 0.5f * dt, nsteps, flags & (B2_POTENTIAL | B2_INIT_ACC),
-                 chunk_size(n, flags & B2_POTENTIAL), nch, sh.I, sh.G, make_watch()};
+                 chunk_size(n, flags & B2_POTENTIAL), nch, sh.I, sh.G, make_watch(), debug_withhold()};
   void* argv[] = {&args};
   if (cudaLaunchCooperativeKernel(fn, sh.ctas, sh.threads, argv, smem, s) != cudaSuccess) {
     cudaGetLastError();

@@ -94,7 +94,17 @@ Watch make_watch() {
 
 using namespace b2;
 
+namespace b2 {
+static std::atomic<int> g_withhold{-1};
+int debug_withhold() { return g_withhold.load(); }
+}  // namespace b2
+
 extern "C" {
+
+int b2_debug_withhold_publish(int cta) {
+  b2::g_withhold.store(cta < 0 ? -1 : cta);
+  return B2_OK;
+}
 
 int b2_set_poll_timeout_ms(long long ms) {
   if (ms <= 0) return B2_EINVAL;

@@ -1,2 +1,3 @@
 mkdir -p gpurun_out
-for b in trace_small trace_small_ldg trace_small trace_small_ldg; do echo "== $b"; ./scripts/$b 4096 40; ./scripts/$b 8192 40; done > gpurun_out/trace_small.log 2>&1
+timeout 900 python -m pytest tests/test_faults_gpu.py tests/test_parity_gpu.py -m gpu -x -q -p no:cacheprovider -k "fault or expired or leapfrog or persistent" > gpurun_out/gputest_faults.log 2>&1
+echo rc=$? >> gpurun_out/gputest_faults.log

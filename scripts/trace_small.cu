@@ -26,6 +26,7 @@ void allow_max_dynamic_smem(const void* fn) {
   cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, device_info().smem_optin);
 }
 Watch make_watch() { return Watch{nullptr, 4000000000ull}; }
+int debug_withhold() { return -1; }
 }  // namespace b2
 
 int main(int argc, char** argv) {
@@ -67,7 +68,7 @@ int main(int argc, char** argv) {
     cudaMemset(pub, 0, small_workspace_bytes(n));
     cudaMemset(trace, 0, tw * 8);
     SmallArgs a{n, pos, vel, acc, pub, reinterpret_cast<unsigned int*>(pub + 2 * n), 1.f / 4096, 1.f / 128,
-                1.f / 256, steps, B2_INIT_ACC, chunk_size(n, 0), nch, sh.I, sh.G, Watch{nullptr, 4000000000ull},
+                1.f / 256, steps, B2_INIT_ACC, chunk_size(n, 0), nch, sh.I, sh.G, Watch{nullptr, 4000000000ull}, -1,
                 trace};
     void* args[] = {&a};
     cudaEventRecord(e0);

@@ -88,6 +88,32 @@ def test_expired_two_plane_ingest_raises_and_context_survives(short_timeout, res
     _context_still_works(restatement)
 
 
+def test_expired_leapfrog_exchange_raises_and_context_survives(short_timeout):
+    """The persistent small-N leapfrog with one CTA that never announces its positions
+    (b2_debug_withhold_publish): the other CTAs' waits expire, Leapfrog.synchronize raises
+    SolomonError naming the kernel, and the next run on the same context is exact again."""
+    import paper_2411_18889_b200 as b2
+    from paper_2411_18889_b200 import _lib
+
+    lib = _lib.load()
+    pos, vel = b2.plummer(4096, 9)
+    try:
+        lib.b2_debug_withhold_publish(3)
+        lf = b2.Leapfrog(pos.clone(), vel.clone(), 2.0 ** -6, 2.0 ** -7)
+        lf.step(2)
+        with pytest.raises(_lib.SolomonError, match="k_leapfrog_small"):
+            lf.synchronize()
+    finally:
+        lib.b2_debug_withhold_publish(-1)
+    _lib.check_fault()  # cleared
+    a = b2.Leapfrog(pos.clone(), vel.clone(), 2.0 ** -6, 2.0 ** -7)
+    a.step(2)
+    b = b2.Leapfrog(pos.clone(), vel.clone(), 2.0 ** -6, 2.0 ** -7, graphs=False)
+    b.step(2)
+    torch.cuda.synchronize()
+    assert torch.equal(a.pos, b.pos) and torch.isfinite(a.pos).all()
+
+
 def test_fault_word_is_sticky_until_cleared(short_timeout):
     """Once one wait gave up, later waits on the device give up at their first poll (one dead
     peer ends every wait within one poll, not one timeout each) until the host clears it."""
