@@ -168,6 +168,13 @@ int b2_kdk_update_publish(int n, const float *pos_in, float *pos_out, float *vel
                           const float *partials, int nchunks, float h_end, float h_begin, float dt,
                           int phases, float *const *peers, int npeers, void *stream);
 
+/* NVLS variant (NVSwitch multicast all-gather): the updated positions are stored
+ * ONCE through mc_out -- the multicast view (b2_mc_bind) of every rank's position
+ * buffer at this rank's slice -- and land in every rank's copy, this one's included. */
+int b2_kdk_update_multicast(int n, const float *pos_in, float *mc_out, float *vel, float *acc,
+                            const float *partials, int nchunks, float h_end, float h_begin, float dt,
+                            int phases, void *stream);
+
 /* Whole single-device leapfrog: nsteps KDK steps of the self-gravitating
  * system pos[n] (acc must hold a(pos) on entry unless B2_INIT_ACC is set;
  * holds a(pos) on exit). Small systems (n <= 64 x SMs, fast arithmetic) run
@@ -261,6 +268,21 @@ int b2_diffusion3d_run(int nx, int ny, int nz, float dx, float dy, float dz, flo
  * when the shape has no plan for it (empty ranges only ask). */
 int b2_diffusion3d_run2_planes(int nx, int ny, int nz, float dx, float dy, float dz, float dt, float kappa,
                                const float *f, float *fn, int p0, int p1, int p2, int p3, void *stream);
+
+/* --- NVLS multicast buffers (NVSwitch) --------------------------
+ * One multicast object spans the ranks' GPUs. Rank 0: b2_mc_create (adds its
+ * device, exports a b2_mc_handle_bytes() fabric handle to send to the others); every
+ * other rank: b2_mc_add_device; after ALL ranks added their device (host barrier):
+ * b2_mc_bind maps this rank's copy (uc) and the multicast view (mc) of `bytes` (a
+ * multiple of b2_mc_granular_bytes). Stores through mc reach every rank's copy. */
+int b2_mc_supported(int device); /* 1: the GPU supports multicast AND this process can
+                                    create an object (reaches the NVSwitch fabric) */
+size_t b2_mc_handle_bytes(void);
+int b2_mc_granular_bytes(size_t bytes, int ndev, size_t *out);
+int b2_mc_create(size_t bytes, int ndev, int device, void *handle, void **binding);
+int b2_mc_add_device(const void *handle, int device, void **binding);
+int b2_mc_bind(void *binding, size_t bytes, void **uc_ptr, void **mc_ptr);
+int b2_mc_release(void *binding);
 
 /* --- Peer memory across processes (multi-GPU fused halo) --- */
 

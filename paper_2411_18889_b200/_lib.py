@@ -51,6 +51,7 @@ SIGNATURES = {
     "b2_calc_acc_partials": (_i, [_i, _p, _i, _p, _f, _i, _p, _p]),
     "b2_kdk_update": (_i, [_i, _p, _p, _p, _p, _i, _f, _f, _f, _i, _p]),
     "b2_kdk_update_publish": (_i, [_i, _p, _p, _p, _p, _p, _i, _f, _f, _f, _i, _p, _i, _p]),
+    "b2_kdk_update_multicast": (_i, [_i, _p, _p, _p, _p, _p, _i, _f, _f, _f, _i, _p]),
     "b2_leapfrog": (_i, [_i, _p, _p, _p, _f, _f, _i, _i, _p, _sz, _p]),
     "b2_leapfrog_workspace_bytes": (_sz, [_i, _i]),
     "b2_diffusion3d": (_i, [_i, _i, _i, _f, _f, _f, _f, _f, _p, _p, _p]),
@@ -65,6 +66,13 @@ SIGNATURES = {
     "b2_diffusion3d_slab_halo2": (_i, [_i, _i, _i, _i, _i, _p, _p, _p, _p, _p, _i, _i, _p]),
     "b2_ipc_handle_bytes": (_sz, []),
     "b2_ipc_export": (_i, [_p, _p, ctypes.POINTER(_sz)]),
+    "b2_mc_supported": (_i, [_i]),
+    "b2_mc_handle_bytes": (_sz, []),
+    "b2_mc_granular_bytes": (_i, [_sz, _i, ctypes.POINTER(_sz)]),
+    "b2_mc_create": (_i, [_sz, _i, _i, _p, ctypes.POINTER(_p)]),
+    "b2_mc_add_device": (_i, [_p, _i, ctypes.POINTER(_p)]),
+    "b2_mc_bind": (_i, [_p, _sz, ctypes.POINTER(_p), ctypes.POINTER(_p)]),
+    "b2_mc_release": (_i, [_p]),
     "b2_ipc_import": (_i, [_p, _sz, ctypes.POINTER(_p)]),
     "b2_ipc_close": (_i, [_p, _sz]),
 }

@@ -20,7 +20,7 @@ CSRC = PKG / "csrc"
 LIB_DIR = PKG / "lib"
 LIB = LIB_DIR / "libsolomon_b200.so"
 PROBE = LIB_DIR / "libsolomon_probe.so"
-SOURCES = ["nbody.cu", "nbody_small.cu", "diffusion.cu", "diffusion_tb2.cu", "diffusion_resident.cu", "diffusion_halo.cu", "dropin.cu", "ipc.cu", "runtime.cu"]
+SOURCES = ["nbody.cu", "nbody_small.cu", "diffusion.cu", "diffusion_tb2.cu", "diffusion_resident.cu", "diffusion_halo.cu", "dropin.cu", "ipc.cu", "multicast.cu", "runtime.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

@@ -371,6 +371,7 @@ constexpr int kMaxPeers = 8;
 struct Peers {
   float4* p[kMaxPeers];
   int n;
+  float4* mc;  // NVLS: the multicast view of every rank's next buffer (this rank's slice), or null
 };
 constexpr int kPublish = 8;  // internal phase bit
 
@@ -427,10 +428,17 @@ __global__ void __launch_bounds__(128)
     vel[i] = v;
   }
   if (drift || publish) {
-    pos_out[i] = x;
+    if (peers.mc) {
+      // one store through the switch lands in every rank's copy, this rank's included
+      asm volatile("multimem.st.relaxed.sys.global.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(peers.mc + i), "f"(x.x),
+                   "f"(x.y), "f"(x.z), "f"(x.w)
+                   : "memory");
+    } else {
+      pos_out[i] = x;
 #pragma unroll
-    for (int k = 0; k < kMaxPeers; ++k)
-      if (k < peers.n) peers.p[k][i] = x;  // peer store over NVLink/NVSwitch
+      for (int k = 0; k < kMaxPeers; ++k)
+        if (k < peers.n) peers.p[k][i] = x;  // peer store over NVLink/NVSwitch
+    }
   }
 }
 
@@ -667,6 +675,24 @@ int b2_kdk_update_publish(int n, const float* pos_in, float* pos_out, float* vel
   k_kdk_update<<<(n + 127) / 128, 128, 0, as_stream(stream)>>>(
       n, reinterpret_cast<const float4*>(pos_in), reinterpret_cast<float4*>(pos_out), reinterpret_cast<float4*>(vel),
       reinterpret_cast<float4*>(acc), reinterpret_cast<const float4*>(partials), nchunks, h_end, h_begin, dt, ph, pp);
+  return launch_status();
+}
+
+int b2_kdk_update_multicast(int n, const float* pos_in, float* mc_out, float* vel, float* acc, const float* partials,
+                            int nchunks, float h_end, float h_begin, float dt, int phases, void* stream) {
+  int rc;
+  if (phases & ~(B2_KDK_REDUCE | B2_KDK_KICK_END | B2_KDK_KICK_DRIFT)) return B2_EINVAL;
+  if ((rc = check_particles(n, acc)) || (rc = check_particles(n, pos_in)) || (rc = check_particles(n, mc_out)))
+    return rc;
+  if ((phases & B2_KDK_REDUCE) && ((rc = check_particles(n, partials)) || nchunks < 1)) return rc ? rc : B2_EINVAL;
+  if ((phases & (B2_KDK_KICK_END | B2_KDK_KICK_DRIFT)) && (rc = check_particles(n, vel))) return rc;
+  if (n <= 0) return B2_OK;
+  Peers pp{};
+  pp.mc = reinterpret_cast<float4*>(mc_out);
+  k_kdk_update<<<(n + 127) / 128, 128, 0, as_stream(stream)>>>(
+      n, reinterpret_cast<const float4*>(pos_in), nullptr, reinterpret_cast<float4*>(vel),
+      reinterpret_cast<float4*>(acc), reinterpret_cast<const float4*>(partials), nchunks, h_end, h_begin, dt,
+      phases | kPublish, pp);
   return launch_status();
 }
 

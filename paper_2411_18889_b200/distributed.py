@@ -119,6 +119,18 @@ def _all_gather_inplace(out: torch.Tensor, local: torch.Tensor, group=None) -> N
     dist.all_gather(parts, local.clone(), group=group)
 
 
+class _CudaArray:
+    """__cuda_array_interface__ of raw device memory, for a zero-copy torch view."""
+
+    def __init__(self, ptr: int, shape: tuple, typestr: str = "<f4"):
+        self.__cuda_array_interface__ = {"shape": shape, "typestr": typestr, "data": (ptr, False), "version": 3,
+                                         "strides": None}
+
+
+def _device_view(ptr: int, shape: tuple, device: torch.device) -> torch.Tensor:
+    return torch.as_tensor(_CudaArray(ptr, shape), device=device)
+
+
 def init_distributed(backend: str = "nccl", timeout_s: float = 600.0) -> tuple[int, int, int]:
     """One process per GPU (torchrun env: RANK, WORLD_SIZE, LOCAL_RANK, MASTER_*).
 
@@ -188,13 +200,18 @@ class ShardedLeapfrog:
     they were recorded). Double buffering removes the write-after-read hazard:
     update k writes the buffer last read by force k-1, and every peer's force k
     waits on all updates k-1, each of which followed that peer's force k-1.
+
+    ``transport="nvls"`` (NVSwitch multicast): the two buffers are every rank's copy of one
+    multicast object (``b2_mc_*``); the update kernel stores each new position ONCE through
+    the multicast view (``b2_kdk_update_multicast``) and the switch writes it into all ranks'
+    copies -- one store per particle instead of one per peer. Ordering as for ``p2p``.
     """
 
     _closed = False  # set by close(): stepping afterwards raises
 
     def __init__(self, pos_local: torch.Tensor, vel_local: torch.Tensor, eps: float, dt: float, *, group=None,
                  kernels=None, potential: bool = False, exact: bool = False, transport: str = "nccl"):
-        if transport not in ("nccl", "p2p"):
+        if transport not in ("nccl", "p2p", "nvls"):
             raise ValueError(f"unknown transport {transport!r}")
         self.group = group
         self.transport = transport
@@ -202,8 +219,11 @@ class ShardedLeapfrog:
         self.plan = shard_plan(n_local * dist.get_world_size(group), group)
         self.k = kernels or CudaNBodyKernels(potential, exact)
         dev = pos_local.device
-        nbuf = 2 if transport == "p2p" else 1
-        self._bufs = [torch.empty((self.plan.n_total, 4), dtype=torch.float32, device=dev) for _ in range(nbuf)]
+        if transport == "nvls":
+            self._bufs = self._setup_nvls(dev)  # the two buffers: this rank's copy of the multicast memory
+        else:
+            nbuf = 2 if transport == "p2p" else 1
+            self._bufs = [torch.empty((self.plan.n_total, 4), dtype=torch.float32, device=dev) for _ in range(nbuf)]
         self._cur = 0
         self.pos.copy_(pos_local)
         self.vel = vel_local.clone()
@@ -223,6 +243,8 @@ class ShardedLeapfrog:
         self.steps = 0
         if transport == "p2p":
             self._setup_p2p()
+        elif transport == "nvls":
+            self._setup_events()
         self.gather()
         self._force()
         if not self.fused:
@@ -291,6 +313,73 @@ class ShardedLeapfrog:
             self.close()
             raise _lib.SolomonError(f"p2p position transport unavailable on some rank: {err or 'peer failure'}")
 
+    # ---- nvls transport (NVSwitch multicast) -----------------------------------
+    def _agree(self, err, what: str) -> None:
+        ok = torch.tensor([0 if err else 1], dtype=torch.int32)
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN, group=self.ctrl)
+        if not int(ok.item()):
+            raise _lib.SolomonError(f"{what} unavailable on some rank: {err or 'peer failure'}")
+
+    def _setup_nvls(self, dev: torch.device) -> list:
+        """Both position buffers in ONE multicast object (b2_mc_*): rank 0 creates it, every
+        rank adds its GPU, then binds its own copy and maps the multicast view. The update
+        kernel stores each new position once through the multicast view
+        (b2_kdk_update_multicast) and the switch writes it into every rank's copy -- the NVLS
+        all-gather. Events and the host barrier order the steps as for p2p."""
+        lib = _lib.load()
+        if dev.type != "cuda":
+            raise ValueError("transport='nvls' needs CUDA tensors")
+        self.ctrl = dist.new_group(backend="gloo") if dist.get_backend(self.group) != "gloo" else self.group
+        world, rank = self.plan.world, self.plan.rank
+        err = None if lib.b2_mc_supported(dev.index) else "no multicast (NVLS) support on this GPU"
+        self._agree(err, "nvls transport")
+        need = 2 * self.plan.n_total * 16
+        size = ctypes.c_size_t(0)
+        _lib.check(lib.b2_mc_granular_bytes(need, world, ctypes.byref(size)), "mc_granular_bytes")
+        binding, handle, err = ctypes.c_void_p(), ctypes.create_string_buffer(lib.b2_mc_handle_bytes()), None
+        if rank == 0:
+            rc = lib.b2_mc_create(size.value, world, dev.index, handle, ctypes.byref(binding))
+            err = None if rc == 0 else f"b2_mc_create: {lib.b2_error_string(rc).decode()} ({rc})"
+        shared = [handle.raw if rank == 0 else None]
+        dist.broadcast_object_list(shared, src=dist.get_global_rank(self.ctrl, 0) if self.ctrl is not None else 0,
+                                   group=self.ctrl)
+        if rank != 0 and shared[0] is not None:
+            h = ctypes.create_string_buffer(shared[0], len(shared[0]))
+            rc = lib.b2_mc_add_device(h, dev.index, ctypes.byref(binding))
+            err = None if rc == 0 else f"b2_mc_add_device: {lib.b2_error_string(rc).decode()} ({rc})"
+        try:
+            self._agree(err, "nvls transport")  # every GPU added before anyone binds
+        except _lib.SolomonError:
+            if binding.value:
+                lib.b2_mc_release(binding)
+            raise
+        uc, mc = ctypes.c_void_p(), ctypes.c_void_p()
+        rc = lib.b2_mc_bind(binding, size.value, ctypes.byref(uc), ctypes.byref(mc))
+        err = None if rc == 0 else f"b2_mc_bind: {lib.b2_error_string(rc).decode()} ({rc})"
+        try:
+            self._agree(err, "nvls transport")
+        except _lib.SolomonError:
+            lib.b2_mc_release(binding)
+            raise
+        self._mc = (binding, uc.value, mc.value)
+        n = self.plan.n_total
+        return [_device_view(uc.value + b * n * 16, (n, 4), dev) for b in range(2)]
+
+    def _setup_events(self) -> None:
+        """The peers' post-update interprocess events (nvls; p2p sets them up with its mappings)."""
+        self.event = torch.cuda.Event(enable_timing=False, interprocess=True)
+        self.event.record(torch.cuda.current_stream(self.pos_all.device))
+        everyone = [None] * self.plan.world
+        dist.all_gather_object(everyone, bytes(self.event.ipc_handle()), group=self.ctrl)
+        self._peers = [([], [], torch.cuda.Event.from_ipc_handle(self.pos_all.device, h))
+                       for r, h in enumerate(everyone) if r != self.plan.rank]
+
+    def _mc_slice(self, buf: int) -> int:
+        """Multicast address of this rank's slice of buffer ``buf``."""
+        if self._closed:
+            raise RuntimeError("ShardedLeapfrog: the nvls transport was closed")
+        return self._mc[2] + (buf * self.plan.n_total + self.plan.lo) * 16
+
     def _peer_ptrs(self, buf: int):
         if self._closed:
             raise RuntimeError("ShardedLeapfrog: the p2p transport was closed")
@@ -301,13 +390,19 @@ class ShardedLeapfrog:
     def _publish_update(self, vel, partials, h_end, h_begin, dt, phases) -> None:
         """Update + store the resulting positions into the next buffer here and on every peer."""
         nxt = 1 - self._cur
-        peers, npeers = self._peer_ptrs(nxt)
-        dst = self._bufs[nxt][self.plan.lo:self.plan.hi]
         ptr = lambda t: t.data_ptr() if t is not None else None  # noqa: E731
-        _lib.check(_lib.load().b2_kdk_update_publish(
-            self.acc.shape[0], self.pos.data_ptr(), dst.data_ptr(), ptr(vel), self.acc.data_ptr(), ptr(partials),
-            self.nch, float(h_end), float(h_begin), float(dt), phases, peers, npeers,
-            _lib.stream_handle(self.acc.device)), "kdk_update_publish")
+        if self.transport == "nvls":
+            _lib.check(_lib.load().b2_kdk_update_multicast(
+                self.acc.shape[0], self.pos.data_ptr(), self._mc_slice(nxt), ptr(vel), self.acc.data_ptr(),
+                ptr(partials), self.nch, float(h_end), float(h_begin), float(dt), phases,
+                _lib.stream_handle(self.acc.device)), "kdk_update_multicast")
+        else:
+            peers, npeers = self._peer_ptrs(nxt)
+            dst = self._bufs[nxt][self.plan.lo:self.plan.hi]
+            _lib.check(_lib.load().b2_kdk_update_publish(
+                self.acc.shape[0], self.pos.data_ptr(), dst.data_ptr(), ptr(vel), self.acc.data_ptr(), ptr(partials),
+                self.nch, float(h_end), float(h_begin), float(dt), phases, peers, npeers,
+                _lib.stream_handle(self.acc.device)), "kdk_update_publish")
         self.event.record(torch.cuda.current_stream(self.acc.device))
         self._cur = nxt
 
@@ -318,7 +413,7 @@ class ShardedLeapfrog:
             stream.wait_event(ev)
 
     def close(self) -> None:
-        if self.transport != "p2p" or self._closed:
+        if self.transport == "nccl" or self._closed:
             return
         self._closed = True
         torch.cuda.synchronize(self.pos_all.device)
@@ -328,6 +423,10 @@ class ShardedLeapfrog:
             for p, off in opened:
                 lib.b2_ipc_close(p, off)
         self._peers = []
+        if self.transport == "nvls":
+            self._bufs = [b.clone() for b in self._bufs]  # keep the state readable after the unmap
+            lib.b2_mc_release(self._mc[0])
+            self._mc = None
         dist.barrier(group=self.ctrl)
 
     # ---- stepping --------------------------------------------------------------
@@ -337,10 +436,15 @@ class ShardedLeapfrog:
             _all_gather_inplace(self.pos_all, self.pos, self.group)
             return
         # publish our slice of the current buffer into every peer's current buffer
-        peers, npeers = self._peer_ptrs(self._cur)
-        _lib.check(_lib.load().b2_kdk_update_publish(
-            self.pos.shape[0], self.pos.data_ptr(), self.pos.data_ptr(), None, self.pos.data_ptr(), None, 1,
-            0.0, 0.0, 0.0, 0, peers, npeers, _lib.stream_handle(self.pos.device)), "publish")
+        if self.transport == "nvls":
+            _lib.check(_lib.load().b2_kdk_update_multicast(
+                self.pos.shape[0], self.pos.data_ptr(), self._mc_slice(self._cur), None, self.pos.data_ptr(), None,
+                1, 0.0, 0.0, 0.0, 0, _lib.stream_handle(self.pos.device)), "publish")
+        else:
+            peers, npeers = self._peer_ptrs(self._cur)
+            _lib.check(_lib.load().b2_kdk_update_publish(
+                self.pos.shape[0], self.pos.data_ptr(), self.pos.data_ptr(), None, self.pos.data_ptr(), None, 1,
+                0.0, 0.0, 0.0, 0, peers, npeers, _lib.stream_handle(self.pos.device)), "publish")
         self.event.record(torch.cuda.current_stream(self.pos.device))
         self._await_peers()
 

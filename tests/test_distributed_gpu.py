@@ -358,3 +358,86 @@ def test_p2p_slab_checkpoint_resume_bit_identical(tmp_path):
     out = tmp_path / "ok.npy"
     mp.spawn(_p2p_ckpt_worker, args=(2, _port(), str(tmp_path / "s.{rank}.pt"), str(out)), nprocs=2, join=True)
     assert np.load(out).all()
+
+
+def _nvls_worker(rank, world, port, n, steps, out):
+    import torch.distributed as dist
+
+    import paper_2411_18889_b200 as b2
+    from paper_2411_18889_b200 import _lib
+    from paper_2411_18889_b200.distributed import ShardedLeapfrog
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    pos, vel = b2.plummer_numpy(n, 8)
+    nl = n // world
+    mk = lambda: ShardedLeapfrog(torch.from_numpy(pos[rank * nl:(rank + 1) * nl]).cuda(),  # noqa: E731
+                                 torch.from_numpy(vel[rank * nl:(rank + 1) * nl]).cuda(), 2.0 ** -6, 2.0 ** -7,
+                                 transport="nvls")
+    res = {}
+    try:
+        sim = mk()
+    except _lib.SolomonError as e:  # every rank must see the same verdict (no one left in a collective)
+        res["error"] = str(e)
+    else:
+        sim.step(steps)
+        sim.step(2)  # re-open after a closed step
+        torch.cuda.synchronize()
+        res.update(p=sim.pos.cpu().numpy(), v=sim.vel.cpu().numpy(), a=sim.acc.cpu().numpy(),
+                   allpos=sim.pos_all.cpu().numpy())
+        sim.close()
+        res["after_close"] = sim.pos_all.cpu().numpy()  # the state stays readable once unmapped
+        try:
+            sim.step(1)
+            res["error"] = "step after close did not raise"
+        except RuntimeError:
+            pass
+    parts = [None] * world
+    dist.all_gather_object(parts, res)
+    if rank == 0:
+        lf = b2.Leapfrog(torch.from_numpy(pos).cuda(), torch.from_numpy(vel).cuda(), 2.0 ** -6, 2.0 ** -7)
+        lf.step(steps)
+        lf.step(2)
+        np.savez(out, errors=np.array([q.get("error", "") for q in parts]),
+                 lp=lf.pos.cpu().numpy(), lv=lf.vel.cpu().numpy(), la=lf.acc.cpu().numpy(),
+                 **({k: np.concatenate([q[k] for q in parts]) for k in ("p", "v", "a")}
+                    if all("p" in q for q in parts) else {}),
+                 **({"allpos": parts[0]["allpos"], "after_close": parts[0]["after_close"]} if "allpos" in parts[0]
+                    else {}))
+    dist.destroy_process_group()
+
+
+def test_nvls_multicast_allgather_leapfrog_matches_single_device(tmp_path):
+    """transport='nvls' (NVSwitch multicast, b2_mc_*): the update kernel stores each position
+    once through the multicast view and it lands in every rank's buffer. World 1 on the one
+    GPU: the whole path (create, add, bind, multimem stores, release) against Leapfrog, bit
+    for bit; skipped where the GPU has no multicast support."""
+    import torch.multiprocessing as mp
+
+    from paper_2411_18889_b200 import _lib
+
+    if not _lib.load().b2_mc_supported(0):
+        pytest.skip("no NVLS multicast object can be created here (GPU or fabric access)")
+    out = tmp_path / "nvls.npz"
+    mp.spawn(_nvls_worker, args=(1, _port(), 8192, 3, str(out)), nprocs=1, join=True)
+    z = np.load(out)
+    assert not any(z["errors"]), z["errors"]
+    for a, b in (("p", "lp"), ("v", "lv"), ("a", "la"), ("allpos", "lp"), ("after_close", "lp")):
+        assert np.array_equal(z[a].view(np.uint32), z[b].view(np.uint32)), a
+
+
+def test_nvls_unavailable_fails_cleanly_on_every_rank(tmp_path):
+    """Where no multicast object can be made -- two ranks on the same GPU, or a process that
+    does not reach the NVSwitch fabric (this container) -- every rank gets the same
+    SolomonError from the constructor (agreed collectively); none hangs."""
+    import torch.multiprocessing as mp
+
+    from paper_2411_18889_b200 import _lib
+
+    worlds = [2] if _lib.load().b2_mc_supported(0) else [1, 2]
+    for world in worlds:
+        out = tmp_path / f"nvls{world}.npz"
+        mp.spawn(_nvls_worker, args=(world, _port(), 8192, 1, str(out)), nprocs=world, join=True)
+        errs = np.load(out)["errors"]
+        assert len(errs) == world and all("nvls transport unavailable" in e for e in errs), errs
