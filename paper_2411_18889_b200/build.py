@@ -51,6 +51,9 @@ def build(force: bool = False, verbose: bool = False) -> pathlib.Path:
            "-Xcompiler", "-fno-fast-math",
            "-DSOLOMON_B200_BUILD", f"-I{ROOT / 'include'}", f"-I{CSRC}",
            *(str(CSRC / s) for s in SOURCES), "-o", str(LIB)]
+    extra = os.environ.get("SOLOMON_NVCC_EXTRA")  # A/B builds of compile-time variants (tuning)
+    if extra:
+        cmd[1:1] = extra.split()
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
     subprocess.run(cmd, check=True)
