@@ -512,6 +512,8 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         full["secondary"] = {"diffusion": run_diffusion(ctx)}
     else:
         full["secondary"] = {}
+    if world == 1 and not sharded:
+        full["secondary"]["nbody_uniform"] = nbody_uniform_leg(ctx, n, fp32_peak)
 
     if world > 1:
         sec = full["secondary"]
@@ -547,6 +549,42 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         except FileNotFoundError as e:
             full["cpu_baseline"] = {"value": None, "unavailable": str(e)}
     return full
+
+
+def nbody_uniform_leg(ctx, n, fp32_peak):
+    """The north star's other particle set: the same force evaluation (k_force_fast with the
+    in-kernel reduction) on N uniform-cube particles, L2 flushed between the timed evaluations,
+    with the same sampled parity check."""
+    import torch
+
+    import paper_2411_18889_b200 as b2
+
+    pos_np, _ = b2.uniform_numpy(n, 42)
+    pos = torch.from_numpy(pos_np).to(ctx.dev)
+    acc = torch.empty_like(pos)
+    ws = b2.workspace(n, n, device=ctx.dev)
+    b2.calc_acc(n, pos, acc, n, pos, EPS, ws=ws)
+    times = []
+    for _ in range(3):
+        ctx.flush.zero_()
+        e0, e1 = ctx.events(2)
+        e0.record(ctx.stream)
+        b2.calc_acc(n, pos, acc, n, pos, EPS, ws=ws)
+        e1.record(ctx.stream)
+        torch.cuda.synchronize(ctx.dev)
+        times.append(e0.elapsed_time(e1))
+    ms = statistics.median(times)
+    tf = FLOP_PER_INTERACTION * float(n) * n / (ms * 1e-3) / 1e12
+    out = {"value": float(n) * n / (ms * 1e-3) / 1e9, "unit": "Ginteractions/s", "n": n,
+           "what": "uniform cube [-1,1]^3, one force evaluation, median of 3",
+           "roofline": {"achieved": tf, "peak": fp32_peak, "frac": tf / fp32_peak}}
+    if not ctx.args.no_cpu_baseline:
+        try:
+            out["parity"] = nbody_sample_parity(pos_np, acc.cpu().numpy(), n_sample=256, what="the uniform-cube force")
+        except FileNotFoundError as e:
+            out["parity"] = {"unavailable": str(e)}
+    del pos, acc, ws
+    return out
 
 
 def guarded(ctx, what: str, fn):
@@ -1051,6 +1089,11 @@ def compact(full: dict) -> dict:
                                     "roofline": _roof(run["roofline"]), "bit_identical": rp.get("bit_identical")}
             for k in ("kernel", "unit", "bound"):
                 sec["diffusion_run"]["roofline"].pop(k, None)
+    u = full.get("secondary", {}).get("nbody_uniform")
+    if u:
+        sec["nbody_uniform"] = {"value": _r(u["value"]), "frac": _r(u["roofline"]["frac"], 3),
+                                **({"relL2_f64": _r(u["parity"]["relL2_f64"], 2), "ok": u["parity"]["ok"]}
+                                   if "relL2_f64" in u.get("parity", {}) else {})}
     for k in ("nbody_p2p", "diffusion_p2p", "scale_anchor"):
         v = full.get("secondary", {}).get(k)
         if v is not None:
