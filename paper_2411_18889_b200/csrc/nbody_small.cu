@@ -277,8 +277,14 @@ __global__ void __launch_bounds__(kSmallMaxThreads, 1) k_leapfrog_small(const Sm
       asm volatile("bar.sync 2, %0;" ::"r"(32 * pubw) : "memory");
     else
       __syncwarp();
-    if (tid == 0 && static_cast<int>(blockIdx.x) != a.withhold)
+    if (tid == 0 && static_cast<int>(blockIdx.x) != a.withhold) {
+#ifdef B2_PROBE_NOFENCE  // timing probe only: the arrival WITHOUT release -- incorrect
+      asm volatile("red.relaxed.gpu.global.add.u32 [%0], %1;" ::"l"(a.arrive + 32 * counter_of(blockIdx.x)), "r"(1u)
+                   : "memory");
+#else
       red_release_add_u32(a.arrive + 32 * counter_of(blockIdx.x), 1u);
+#endif
+    }
   };
   // this warp: wait until the CTAs on the counters of its slice's producers published `state`
   auto slice_published = [&](int state) -> bool {
