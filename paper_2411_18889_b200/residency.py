@@ -1,7 +1,7 @@
 """Data-residency helpers: the caller side of the kernels' ``present(f, fn)`` contract.
 
 Mirrors Solomon's intuitive data directives (the reference's
-catalog ``pkg/src/pragmaport/data/mappings.reg:74-104``) as thin torch
+catalog ``pkg/src/pragmaport/data/mappings.reg:74-104,345-347,366-367``) as thin torch
 utilities over host numpy arrays:
 
 ==========================  =========================================  ==================
@@ -12,6 +12,8 @@ FREE_FROM_DEVICE(a, ...)    acc exit data delete(a, ...)               free_from
 MEMCPY_H2D(a, ...)          acc update device(a, ...)                  memcpy_h2d
 MEMCPY_D2H(a, ...)          acc update host(a, ...)                    memcpy_d2h
 DATA_ACCESS_BY_DEVICE(...)  acc data ...                               data_access_by_device
+DATA_ACCESS_BY_HOST(...)    acc host_data ... (use_device)             data_access_by_host
+USE_DEVICE_DATA_FROM_HOST   acc host_data use_device(a, ...)           use_device_data_from_host
 (present clause)            present(a)                                 present
 SYNCHRONIZE()               acc wait                                   synchronize
 ==========================  =========================================  ==================
@@ -129,3 +131,19 @@ def data_access_by_device(copyin=(), copyout=(), copy=(), create=()):
         memcpy_d2h(*[a for a in (*copyout, *copy) if _refcount(a) == 1])
     finally:
         free_from_device(*arrays)
+
+
+@contextlib.contextmanager
+def data_access_by_host(*arrays: np.ndarray):
+    """DATA_ACCESS_BY_HOST / USE_DEVICE_DATA_FROM_HOST (``acc host_data use_device(a, ...)``,
+    ``omp target data use_device_ptr(a, ...)``, mappings.reg:345-347,366-367):
+    inside the region host code addresses the DEVICE copies of present arrays -- to hand them
+    to a library or a drop-in call that takes device pointers. Yields the device tensors in
+    argument order (one tensor for one array). Every array must already be present (an
+    enclosing DATA_ACCESS_BY_DEVICE or MALLOC_ON_DEVICE), as ``use_device`` requires; the
+    region moves no data."""
+    mirrors = tuple(present(a) for a in arrays)
+    yield mirrors[0] if len(mirrors) == 1 else mirrors
+
+
+use_device_data_from_host = data_access_by_host

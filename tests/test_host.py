@@ -90,6 +90,9 @@ def test_residency_requires_mapping():
         R.present(a)
     with pytest.raises(b2.SolomonError):
         R.free_from_device(a)
+    with pytest.raises(b2.SolomonError):  # DATA_ACCESS_BY_HOST (use_device) needs a present array
+        with R.data_access_by_host(a):
+            pass
     if not torch.cuda.is_available():
         with pytest.raises(b2.SolomonError):
             R.malloc_on_device(a)

@@ -352,6 +352,23 @@ def test_residency_helpers_present_contract(b2, golden):
         R.present(f0)
 
 
+def test_residency_data_access_by_host_use_device(b2, golden, restatement):
+    """DATA_ACCESS_BY_HOST (acc host_data use_device): inside a device data region the host
+    passes the device copies to the drop-in; copy-out at the region's end brings the step back."""
+    from paper_2411_18889_b200 import residency as R
+
+    f0 = np.ascontiguousarray(golden["diff/cube16/f0"]).copy()
+    dx, dy, dz, dt, kappa = (float(v) for v in golden["diff/cube16/params"])
+    fn = np.zeros_like(f0)
+    with R.data_access_by_device(copyin=[f0], copyout=[fn]):
+        with R.data_access_by_host(f0, fn) as (df, dfn):
+            assert df.is_cuda and dfn.is_cuda
+            b2.diffusion3d(*f0.shape, dx, dy, dz, dt, kappa, df, dfn)
+        with R.use_device_data_from_host(fn) as dfn1:
+            assert dfn1.data_ptr() == dfn.data_ptr()
+    assert bits_equal(fn, restatement.diffusion3d(f0, dx, dy, dz, dt, kappa))
+
+
 def test_residency_nested_regions_present_or_copy(b2):
     """a nested DATA_ACCESS_BY_DEVICE on an array already present only adds a
     reference (OpenACC present_or_copy): no copy-in over newer device data, no early copy-out."""
