@@ -374,7 +374,9 @@ int plan_tb2_tune(int nx, int ny, int nz, const Coefs& c, const float* f, float*
     cudaGetLastError();
     return B2_OK;  // model pick, not cached: a later uncaptured plan call may still tune
   }
-  constexpr int kCandidates = 4;
+  // the model's best few plans, each timed in three interleaved rounds (two launches after a
+  // warm-up), the minimum per plan kept: a single round was within the noise between plans
+  constexpr int kCandidates = 4, kRounds = 3;
   cudaEvent_t ev[2];
   cudaError_t e;
   if ((e = cudaEventCreate(&ev[0])) != cudaSuccess) return static_cast<int>(e);
@@ -382,22 +384,29 @@ int plan_tb2_tune(int nx, int ny, int nz, const Coefs& c, const float* f, float*
     cudaEventDestroy(ev[0]);
     return static_cast<int>(e);
   }
-  float best_ms = 1e30f;
-  for (size_t i = 0; i < cand.size() && i < static_cast<size_t>(kCandidates); ++i) {
-    const TB2Plan& p = cand[i].second;
-    if (launch_tb2(p, nx, ny, nz, c, f, fn, s)) continue;  // warm-up (smem opt-in, caches)
-    cudaEventRecord(ev[0], s);
-    for (int r = 0; r < 2; ++r) launch_tb2(p, nx, ny, nz, c, f, fn, s);
-    cudaEventRecord(ev[1], s);
-    float ms = 0.f;
-    if (cudaEventSynchronize(ev[1]) != cudaSuccess || cudaEventElapsedTime(&ms, ev[0], ev[1]) != cudaSuccess) {
-      cudaGetLastError();
-      continue;
+  const size_t nc = std::min(cand.size(), static_cast<size_t>(kCandidates));
+  std::vector<float> tmin(nc, 1e30f);
+  for (int round = 0; round < kRounds; ++round) {
+    for (size_t i = 0; i < nc; ++i) {
+      const TB2Plan& p = cand[i].second;
+      if (launch_tb2(p, nx, ny, nz, c, f, fn, s)) continue;  // warm-up (smem opt-in, caches)
+      cudaEventRecord(ev[0], s);
+      for (int r = 0; r < 2; ++r) launch_tb2(p, nx, ny, nz, c, f, fn, s);
+      cudaEventRecord(ev[1], s);
+      float ms = 0.f;
+      if (cudaEventSynchronize(ev[1]) != cudaSuccess || cudaEventElapsedTime(&ms, ev[0], ev[1]) != cudaSuccess) {
+        cudaGetLastError();
+        continue;
+      }
+      tmin[i] = std::min(tmin[i], ms / 2);
     }
-    tb2_report("ms", nx, ny, nz, p, ms / 2);
-    if (ms < best_ms) {
-      best_ms = ms;
-      best = p;
+  }
+  float best_ms = 1e30f;
+  for (size_t i = 0; i < nc; ++i) {
+    tb2_report("ms", nx, ny, nz, cand[i].second, tmin[i]);
+    if (tmin[i] < best_ms) {
+      best_ms = tmin[i];
+      best = cand[i].second;
     }
   }
   cudaEventDestroy(ev[0]);
