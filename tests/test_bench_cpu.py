@@ -83,3 +83,25 @@ def test_parity_checkers_accept_the_reference_and_reject_perturbations():
     off[2, 3, 4] = np.nextafter(off[2, 3, 4], np.float32(2))
     r = bench.diffusion_parity(f0, off, 3, args)
     assert not r["bit_identical"] and r["relL2"] > 0
+
+
+def test_compact_line_keeps_the_contract_keys():
+    """The driver keeps only the tail of stdout: compact() of a real full record (the committed
+    round-2 detail file) carries every contract key in a short line."""
+    sys.path.insert(0, str(ROOT))
+    import bench
+
+    full = json.loads((ROOT / "profiles" / "r02" / "bench_detail_r02k.json").read_text())
+    line = json.dumps(bench.compact(full))
+    assert len(line) < 4096
+    d = json.loads(line)
+    for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better", "scaling",
+              "vs_baseline", "dtype", "data", "config", "gpu_launches", "clocks", "roofline", "cpu_baseline", "e2e"):
+        assert k in d, k
+    assert {"bound", "achieved", "peak", "unit", "frac", "traffic"} <= set(d["roofline"])
+    assert {"value", "unit", "h2d_bytes_per_step", "d2h_bytes_per_step"} <= set(d["e2e"])
+    assert {"value", "unit", "cores", "kind", "sample"} <= set(d["cpu_baseline"])
+    sec = d["secondary"]
+    assert sec["diffusion"]["roofline"]["bound"] == "hbm" and sec["diffusion"]["bit_identical"] is True
+    assert sec["diffusion_run"]["bit_identical"] is True and sec["nbody_uniform"]["ok"] is True
+    assert "config0" in sec and "config1" in sec
